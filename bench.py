@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 morphology hot path (driver contract in the task statement).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg2]
+
+Default workload = BASELINE.json configs[1] ("cfg2"), the config the metric is quoted on:
+erosion AND dilation of one 4096x4096 u8 image (top half uniform random, bottom half a binary
+mask of 400 seeded rectangles) for every window of the sweep {3,7,15,31,63,101}^2, 31x1, 1x31.
+One step = those 16 operations. value = output Gpixel/s of the whole job (all ranks).
+
+Inputs are resident in HBM before the timed region; every operation of a step reads a different
+input copy and writes a different output buffer out of 32 rotating pairs (1 GiB total, > 8x the
+126 MB L2), so no operation is served from L2 by its predecessor. Device time is measured with
+CUDA events on the launching stream; multi-GPU time is the max over ranks.
+
+Other workloads (for profiling / the scaling run): cfg1, cfg3 (transposes), cfg4 (512 x 1024^2
+u16 opening 21x21, batch sharded over ranks), cfg5 (32768^2 u8 dilation 63x63, row bands +
+halo exchange over NCCL).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2002_09474_b200.synth import CFG2_WINDOWS, cfg2_image, generate  # noqa: E402
+
+METRIC = "erosion/dilation Gpixel/s (uint8, per window size) and achieved HBM GB/s vs peak"
+ERODE, DILATE, OPEN, CLOSE, GRADIENT = 0, 1, 2, 3, 4
+FALLBACK_HBM_GBS = 6650.0
+
+
+# ---------------------------------------------------------------------------------------------
+def parse_args(argv=None):
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--soak-seconds", type=float, default=1.5)
+    return p.parse_args(argv)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md, MEASURED_PEAKS.json absent)"
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend="nccl"):
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg is not None:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if self.pg is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg is not None:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the GPU is loaded (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.file = None
+
+    def start(self):
+        try:
+            self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.file, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.file.flush()
+        rows = []
+        with open(self.file.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 10:
+                    continue
+                try:
+                    rows.append(dict(sm=float(parts[1]), smax=float(parts[2]), util=float(parts[4]),
+                                     hw=parts[6], hwt=parts[7], swt=parts[8], pcap=parts[9]))
+                except ValueError:
+                    continue
+        os.unlink(self.file.name)
+        loaded = [r for r in rows if r["util"] >= 50] or rows
+        reasons = set()
+        for r in loaded:
+            for key, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"), ("swt", "sw_thermal_slowdown"),
+                              ("pcap", "sw_power_cap")):
+                if r[key].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([r["sm"] for r in loaded]) if loaded else None,
+                "sm_max_mhz": max(r["smax"] for r in loaded) if loaded else None,
+                "reasons": sorted(reasons), "samples": len(loaded)}
+
+
+# ---------------------------------------------------------------------------------------------
+# Workloads. Each exposes: ops (list of (label, launch_fn, algorithmic_bytes, out_pixels)),
+# e2e_step() -> (h2d, d2h) bytes, ref_step(nthreads) for the CPU legs, config dict.
+# ---------------------------------------------------------------------------------------------
+class Cfg2:
+    name = "cfg2"
+    dtype = "u8"
+    NB = 32  # rotating input/output pairs (32 x 2 x 16 MiB = 1 GiB)
+
+    def __init__(self, dist: Dist):
+        self.dist = dist
+        self.img = cfg2_image()
+        self.size = self.img.shape[0]
+        self.ops_list = [(wx, wy, op) for (wx, wy) in CFG2_WINDOWS for op in (ERODE, DILATE)]
+
+    def setup_device(self):
+        import torch
+        import paper_2002_09474_b200 as pkg
+        self.pkg = pkg
+        base = torch.from_numpy(self.img).cuda()
+        self.inputs = [base.clone() for _ in range(self.NB)]
+        self.outputs = [torch.empty_like(base) for _ in range(self.NB)]
+        self.cursor = 0
+        n = self.size * self.size
+        self.ops = []
+        for (wx, wy, op) in self.ops_list:
+            self.ops.append((f"{'erode' if op == ERODE else 'dilate'} {wx}x{wy}", (wx, wy, op), 2 * n, n))
+
+    def launch(self, spec):
+        wx, wy, op = spec
+        i = self.cursor % self.NB
+        self.cursor += 1
+        self.pkg.morph_device(self.inputs[i], self.outputs[i], wx, wy, op)
+
+    def config(self):
+        return {"workload": "cfg2: 4096x4096 u8, erode+dilate per window, windows "
+                            + ",".join(f"{a}x{b}" for a, b in CFG2_WINDOWS),
+                "image": "4096x4096 u8: rows 0-2047 seeded uniform (splitmix64 seed 2), rows 2048-4095 "
+                         "0/255 mask of 400 seeded rectangles side 5-200",
+                "ops_per_step": len(self.ops_list), "border": "replicate",
+                "l2": "no flush: 32 rotating input/output buffer pairs (1 GiB) >> 126 MB L2",
+                "parallelism": f"replicas x{self.dist.world} (independent images, no collective)"}
+
+    def e2e_setup(self):
+        import torch
+        self.h_in = torch.from_numpy(self.img).pin_memory()
+        self.h_out = torch.empty_like(self.h_in).pin_memory()
+
+    def e2e_step(self):
+        import ctypes as C
+        L = self.pkg.lib()
+        n = self.size
+        h2d = d2h = 0
+        for (wx, wy, op) in self.ops_list:
+            rc = L.rmgpu_morph_host_u8(C.c_void_p(self.h_in.data_ptr()), n, C.c_void_p(self.h_out.data_ptr()), n,
+                                       n, n, wx, wy, op, 0, 0, 0, 0)
+            if rc:
+                raise RuntimeError(f"rmgpu_morph_host_u8 failed: {rc} {L.rmgpu_last_error()}")
+            h2d += n * n
+            d2h += n * n
+        return h2d, d2h
+
+    def out_pixels_per_step(self):
+        return len(self.ops_list) * self.size * self.size
+
+    # CPU legs (reference code, oracle/_ref): one full step = the same 16 operations
+    def ref_step(self, R, nthreads, out):
+        for (wx, wy, op) in self.ops_list:
+            R.morph(self.img, wx, wy, op, nthreads=nthreads, out=out)
+        return self.out_pixels_per_step()
+
+
+class Cfg1(Cfg2):
+    name = "cfg1"
+
+    def __init__(self, dist: Dist):
+        self.dist = dist
+        self.img = generate(1920, 1080, 1)
+        self.ops_list = [(3, 3, ERODE), (3, 3, DILATE)]
+
+    def setup_device(self):
+        import torch
+        import paper_2002_09474_b200 as pkg
+        self.pkg = pkg
+        base = torch.from_numpy(self.img).cuda()
+        self.NB = 64
+        self.inputs = [base.clone() for _ in range(self.NB)]
+        self.outputs = [torch.empty_like(base) for _ in range(self.NB)]
+        self.cursor = 0
+        n = self.img.size
+        self.ops = [(f"{'erode' if op == ERODE else 'dilate'} 3x3", (wx, wy, op), 2 * n, n)
+                    for (wx, wy, op) in self.ops_list]
+
+    def config(self):
+        return {"workload": "cfg1: 1920x1080 u8 erode+dilate 3x3 (seed 1)", "border": "replicate",
+                "l2": "no flush: 64 rotating buffer pairs (265 MB) > L2",
+                "parallelism": f"replicas x{self.dist.world}"}
+
+    def e2e_step(self):
+        import ctypes as C
+        L = self.pkg.lib()
+        h, w = self.img.shape
+        for (wx, wy, op) in self.ops_list:
+            rc = L.rmgpu_morph_host_u8(C.c_void_p(self.h_in.data_ptr()), w, C.c_void_p(self.h_out.data_ptr()), w,
+                                       w, h, wx, wy, op, 0, 0, 0, 0)
+            if rc:
+                raise RuntimeError(rc)
+        return 2 * self.img.size, 2 * self.img.size
+
+    def out_pixels_per_step(self):
+        return 2 * self.img.size
+
+
+WORKLOADS = {"cfg1": Cfg1, "cfg2": Cfg2}
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference_arm(args, dist: Dist):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref, compiled from the
+    reference sources) on the host cores, same workload/metric. Rank 0 only."""
+    if dist.rank != 0:
+        return 0
+    import oracle
+    wl = WORKLOADS[args.workload](dist)
+    if not oracle.Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/librmref.so not built"}))
+        return 0
+    R = oracle.reference()
+    nthreads = os.cpu_count() or 1
+    out = np.empty_like(wl.img)
+    for _ in range(args.warmup):
+        wl.ref_step(R, nthreads, out)
+    t0 = time.perf_counter()
+    px = 0
+    for _ in range(args.steps):
+        px += wl.ref_step(R, nthreads, out)
+    dt = time.perf_counter() - t0
+    value = px / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype,
+            "data": "synthetic (seeded generator, SURVEY.md 8d)", "config": wl.config(),
+            "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": nthreads, "kind": "reference",
+                             "sample": f"full workload per step; reference rectmorph (oracle/_ref, -O3, "
+                                       f"DispatchConfig paper 69/59) on {nthreads} threads via row bands"},
+            "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline(wl) -> dict | None:
+    try:
+        import oracle
+        if not oracle.Reference.available():
+            return None
+        R = oracle.reference()
+    except Exception:
+        return None
+    nthreads = os.cpu_count() or 1
+    out = np.empty_like(wl.img)
+    wl.ref_step(R, nthreads, out)  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    px = 0
+    while True:
+        px += wl.ref_step(R, nthreads, out)
+        reps += 1
+        if time.perf_counter() - t0 > 3.0 or reps >= 5:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": nthreads, "kind": "reference",
+            "sample": f"{reps} full step(s) of {wl.name} through the reference rectmorph (oracle/_ref) on "
+                      f"{nthreads} host threads (row bands + halo), paper DispatchConfig"}
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    dist = Dist()
+    if args.impl == "reference":
+        return run_reference_arm(args, dist)
+
+    import torch
+    import paper_2002_09474_b200 as pkg
+    torch.cuda.set_device(dist.local)
+    dist.init("nccl")
+    wl = WORKLOADS[args.workload](dist)
+    wl.setup_device()
+    stream = torch.cuda.current_stream()
+    peak, peak_src = peaks()
+
+    def step():
+        for (_, spec, _, _) in wl.ops:
+            wl.launch(spec)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < args.soak_seconds:  # keep the GPU loaded for the sampler
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize()
+
+    nops = len(wl.ops)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps * nops + 1)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = pkg.launch_count()
+    evs[0].record(stream)
+    k = 0
+    for _ in range(args.steps):
+        for (_, spec, _, _) in wl.ops:
+            wl.launch(spec)
+            k += 1
+            evs[k].record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = pkg.launch_count() - launches0
+    clocks = sampler.stop()
+
+    total_ms = evs[0].elapsed_time(evs[-1])
+    max_ms = dist.max(total_ms)
+    ms_per_step = max_ms / args.steps
+    value = dist.world * wl.out_pixels_per_step() * args.steps / (max_ms / 1e3) / 1e9
+
+    # per-op durations (event pairs around each launch on the launching stream)
+    durs = {}
+    for i in range(1, k + 1):
+        label, _, nbytes, npx = wl.ops[(i - 1) % nops]
+        durs.setdefault(label, []).append((evs[i - 1].elapsed_time(evs[i]), nbytes, npx))
+    per_window = []
+    tot_b = tot_t = 0.0
+    for label, vals in durs.items():
+        ms = statistics.median(v[0] for v in vals)
+        nbytes, npx = vals[0][1], vals[0][2]
+        tot_b += sum(v[1] for v in vals)
+        tot_t += sum(v[0] for v in vals)
+        per_window.append({"op": label, "us": round(ms * 1e3, 2), "gpix_s": round(npx / (ms / 1e3) / 1e9, 1),
+                           "gb_s": round(nbytes / (ms / 1e3) / 1e9, 1),
+                           "frac": round(nbytes / (ms / 1e3) / 1e9 / peak, 3)})
+    achieved = tot_b / (tot_t / 1e3) / 1e9
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{wl.name}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    e2e = None
+    if not args.no_e2e:
+        wl.e2e_setup()
+        wl.e2e_step()  # warm host pool / pinned paths
+        dist.barrier()
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for _ in range(args.steps):
+            a, b = wl.e2e_step()
+            h2d, d2h = a, b
+        e2e_s = dist.max(time.perf_counter() - t0)
+        e2e = {"value": dist.world * wl.out_pixels_per_step() * args.steps / e2e_s / 1e9, "unit": "Gpixel/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "C-ABI rmgpu_morph_host_u8 per op (pinned host buffers, H2D + kernel + D2H, synchronous)"}
+
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl)
+
+    if dist.rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": dist.world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": wl.dtype,
+                "data": "synthetic (seeded counter-based generator, SURVEY.md 8d; no dataset named)",
+                "config": wl.config(),
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": traffic,
+                             "kernel": "fused separable morph (all launches of the step)",
+                             "algorithmic_bytes": "1 read + 1 write per output pixel",
+                             "peak_source": peak_src},
+                "per_window": per_window,
+                "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+                "plans": {lab: pkg.plan_name(1, 4096, 4096, spec[0], spec[1], spec[2]) for lab, spec, _, _ in wl.ops}
+                if wl.name == "cfg2" else None}
+        print(json.dumps(line))
+    dist.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

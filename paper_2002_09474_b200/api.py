@@ -1,0 +1,372 @@
+"""Python mirror of the reference ``rectmorph`` operator API over the GPU C-ABI.
+
+Names, argument meaning and error behaviour follow the reference's public headers
+(/root/reference/proj/core/include/rectmorph/*.hpp) so the parity tests read like the
+reference's own tests:
+
+* host level (numpy in, numpy out, value semantics): ``erode``, ``dilate``, ``opening``,
+  ``closing``, ``gradient``, ``morph_separable``, ``horizontal_pass``, ``vertical_pass_direct``,
+  ``vertical_pass_via_transpose``, ``transpose_image``, ``transpose_tile``,
+  ``linear_window_1d``, ``van_herk_1d``, ``resolve``, ``make_se``;
+* device level (torch CUDA tensors, stream-ordered, no copies): ``morph_device``,
+  ``morph_batched_device``, ``morph_band_device``, ``transpose_device``,
+  ``transpose_tiles_device``, ``generate_device``.
+
+Errors raise ``Error`` carrying the reference's ``Errc`` (error.hpp:10-22) or ``GpuError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+
+from ._native import lib
+
+
+class Errc(IntEnum):
+    ZeroExtent = 0
+    EvenExtent = 1
+    UnsupportedTile = 2
+    BadMagic = 3
+    BadHeader = 4
+    UnsupportedMaxval = 5
+    TruncatedData = 6
+    BadConfig = 7
+    InsufficientReps = 8
+    IoError = 9
+    BadArgument = 10
+
+
+class Error(RuntimeError):
+    """rectmorph::Error (error.hpp:24-33)."""
+
+    def __init__(self, code: Errc, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+class GpuError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"[{status}] {message}")
+        self.status = status
+
+
+class OpKind(IntEnum):
+    Erode = 0
+    Dilate = 1
+
+
+class PassAlgorithm(IntEnum):
+    Auto = 0
+    Linear = 1
+    VanHerk = 2
+
+
+class VerticalStrategy(IntEnum):
+    Direct = 0
+    ViaTranspose = 1
+
+
+class Axis(IntEnum):
+    Horizontal = 0
+    Vertical = 1
+
+
+# C-ABI op codes (rmgpu.h)
+ERODE, DILATE, OPEN, CLOSE, GRADIENT = 0, 1, 2, 3, 4
+REPLICATE, CONSTANT = 0, 1
+
+
+@dataclass(frozen=True)
+class BorderPolicy:
+    mode: int = REPLICATE
+    value: int = 0
+
+    @staticmethod
+    def replicate() -> "BorderPolicy":
+        return BorderPolicy(REPLICATE, 0)
+
+    @staticmethod
+    def constant(v: int) -> "BorderPolicy":
+        return BorderPolicy(CONSTANT, int(v))
+
+
+@dataclass(frozen=True)
+class StructuringElement:
+    width: int = 1
+    height: int = 1
+
+    @property
+    def wing_x(self) -> int:
+        return self.width // 2
+
+    @property
+    def wing_y(self) -> int:
+        return self.height // 2
+
+
+@dataclass
+class DispatchConfig:
+    threshold_h: int = 69
+    threshold_v: int = 59
+    source: str = "paper"
+
+
+def identity_value(op: OpKind, dtype=np.uint8) -> int:
+    return int(np.iinfo(dtype).max) if op == OpKind.Erode else 0
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().rmgpu_last_error().decode(errors="replace")
+    if 1 <= rc <= 11:
+        raise Error(Errc(rc - 1), msg)
+    raise GpuError(rc, msg or lib().rmgpu_status_string(rc).decode())
+
+
+def make_se(width: int, height: int) -> StructuringElement:
+    """image.cpp:18-24."""
+    if width < 1 or height < 1:
+        raise Error(Errc.ZeroExtent, "structuring element extents must be >= 1")
+    if width % 2 == 0 or height % 2 == 0:
+        raise Error(Errc.EvenExtent, "structuring element extents must be odd")
+    return StructuringElement(width, height)
+
+
+def _validate_window(window: int) -> None:
+    if window < 1:
+        raise Error(Errc.ZeroExtent, "window extent must be >= 1")
+    if window % 2 == 0:
+        raise Error(Errc.EvenExtent, "window extent must be odd")
+
+
+def resolve(algo: PassAlgorithm, window: int, axis: Axis, cfg: DispatchConfig | None = None) -> PassAlgorithm:
+    cfg = cfg or DispatchConfig()
+    return PassAlgorithm(lib().rmgpu_resolve(int(algo), window, int(axis), cfg.threshold_h, cfg.threshold_v))
+
+
+# ------------------------------------------------------------------------------------------
+# host level
+# ------------------------------------------------------------------------------------------
+def _host_image(img: np.ndarray) -> np.ndarray:
+    img = np.asarray(img)
+    if img.ndim != 2 or img.dtype not in (np.uint8, np.uint16):
+        raise Error(Errc.BadArgument, "expected a 2-D uint8 or uint16 image")
+    return np.ascontiguousarray(img)
+
+
+def _morph_host(img: np.ndarray, se: StructuringElement, border: BorderPolicy, op: int) -> np.ndarray:
+    img = _host_image(img)
+    h, w = img.shape
+    out = np.empty_like(img)
+    es = img.itemsize
+    fn = lib().rmgpu_morph_host_u8 if es == 1 else lib().rmgpu_morph_host_u16
+    _check(fn(img.ctypes.data, w * es, out.ctypes.data, w * es, w, h, se.width, se.height, op,
+              border.mode, border.value, 0, 0))
+    return out
+
+
+def erode(img, se, border=BorderPolicy(), cfg=None):
+    return _morph_host(img, se, border, ERODE)
+
+
+def dilate(img, se, border=BorderPolicy(), cfg=None):
+    return _morph_host(img, se, border, DILATE)
+
+
+def opening(img, se, border=BorderPolicy(), cfg=None):
+    return _morph_host(img, se, border, OPEN)
+
+
+def closing(img, se, border=BorderPolicy(), cfg=None):
+    return _morph_host(img, se, border, CLOSE)
+
+
+def gradient(img, se, border=BorderPolicy(), cfg=None):
+    return _morph_host(img, se, border, GRADIENT)
+
+
+def morph_separable(img, op: OpKind, se, border=BorderPolicy(), h_algo=PassAlgorithm.Auto,
+                    v_algo=PassAlgorithm.Auto, v_strategy=None):
+    _validate_window(se.width)
+    _validate_window(se.height)
+    return _morph_host(img, se, border, int(op))
+
+
+def _pass(which: int, img, op: OpKind, window: int, border: BorderPolicy) -> np.ndarray:
+    _validate_window(window)
+    img = _host_image(img)
+    if img.dtype != np.uint8:
+        raise Error(Errc.BadArgument, "pass-level API is 8-bit like the reference")
+    h, w = img.shape
+    out = np.empty_like(img)
+    _check(lib().rmgpu_pass_host_u8(which, img.ctypes.data, w, out.ctypes.data, w, w, h, window, int(op),
+                                    border.mode, border.value, 0))
+    return out
+
+
+def horizontal_pass(img, op, window, border=BorderPolicy(), algo=PassAlgorithm.Auto):
+    return _pass(0, img, op, window, border)
+
+
+def vertical_pass_direct(img, op, window, border=BorderPolicy()):
+    return _pass(1, img, op, window, border)
+
+
+def vertical_pass_via_transpose(img, op, window, border=BorderPolicy(), algo=PassAlgorithm.Auto):
+    return _pass(2, img, op, window, border)
+
+
+def transpose_image(img: np.ndarray) -> np.ndarray:
+    img = _host_image(img)
+    h, w = img.shape
+    out = np.empty((w, h), dtype=img.dtype)
+    es = img.itemsize
+    fn = lib().rmgpu_transpose_host_u8 if es == 1 else lib().rmgpu_transpose_host_u16
+    _check(fn(img.ctypes.data, w * es, out.ctypes.data, h * es, w, h))
+    return out
+
+
+def transpose_tile(data: np.ndarray, stride: int, n: int, offset: int = 0) -> None:
+    """In-place n x n tile transpose (transpose.hpp:36-38); ``data`` is a flat numpy buffer."""
+    if not data.flags.c_contiguous:
+        raise Error(Errc.BadArgument, "tile buffer must be contiguous")
+    ptr = data.ctypes.data + offset * data.itemsize
+    _check(lib().rmgpu_transpose_tiles_host(ptr, data.itemsize, 1, n, stride, 0))
+
+
+def transpose_tiles(data: np.ndarray, n: int) -> None:
+    """In-place transpose of a flat batch of contiguous n x n tiles."""
+    if not data.flags.c_contiguous:
+        raise Error(Errc.BadArgument, "tile buffer must be contiguous")
+    _check(lib().rmgpu_transpose_tiles_host(data.ctypes.data, data.itemsize, data.size // (n * n), n, n, n * n))
+
+
+@dataclass
+class OpCounter:
+    comparisons: int = 0
+
+    def reset(self) -> None:
+        self.comparisons = 0
+
+
+def _window_1d(sig, window, op, border, counter, vanherk):
+    _validate_window(window)
+    sig = np.ascontiguousarray(sig, dtype=np.uint8)
+    if counter is not None:
+        counter.reset()
+    out = np.empty_like(sig)
+    n = sig.size
+    if n == 0:
+        return out
+    if window == 1:
+        out[:] = sig
+        return out
+    _check(lib().rmgpu_window_1d_host_u8(sig.ctypes.data, n, window, int(op), border.mode, border.value,
+                                         2 if vanherk else 1, out.ctypes.data))
+    if counter is not None:  # closed form of the reference algorithm (sliding_extrema.cpp:131,139)
+        if vanherk:
+            ln = n + window - 1
+            counter.comparisons = 2 * (ln - (ln + window - 1) // window) + n
+        else:
+            counter.comparisons = (window - 1) * n
+    return out
+
+
+def linear_window_1d(sig, window, op, border=BorderPolicy(), counter=None):
+    return _window_1d(sig, window, op, border, counter, False)
+
+
+def van_herk_1d(sig, window, op, border=BorderPolicy(), counter=None):
+    return _window_1d(sig, window, op, border, counter, True)
+
+
+# ------------------------------------------------------------------------------------------
+# device level (torch CUDA tensors); pitch = tensor.stride(0) * itemsize
+# ------------------------------------------------------------------------------------------
+def _dev(t):
+    import torch
+    if not t.is_cuda:
+        raise Error(Errc.BadArgument, "expected a CUDA tensor")
+    if t.dtype not in (torch.uint8, torch.uint16):
+        raise Error(Errc.BadArgument, "expected uint8 or uint16")
+    if t.stride(-1) != 1:
+        raise Error(Errc.BadArgument, "rows must be contiguous")
+    return t
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def morph_device(src, dst, wx: int, wy: int, op: int, border: int = REPLICATE, value: int = 0,
+                 stream=None) -> None:
+    """2-D tensors [H, W] (row pitch from stride(0)). Asynchronous on ``stream``."""
+    _dev(src), _dev(dst)
+    h, w = src.shape
+    es = src.element_size()
+    fn = lib().rmgpu_morph_u8 if es == 1 else lib().rmgpu_morph_u16
+    _check(fn(src.data_ptr(), src.stride(0) * es, dst.data_ptr(), dst.stride(0) * es, w, h, wx, wy, op,
+              border, value, 0, 0, _stream_ptr(stream)))
+
+
+def morph_batched_device(src, dst, wx, wy, op, border=REPLICATE, value=0, stream=None) -> None:
+    """3-D tensors [B, H, W]."""
+    _dev(src), _dev(dst)
+    b, h, w = src.shape
+    es = src.element_size()
+    fn = lib().rmgpu_morph_batched_u8 if es == 1 else lib().rmgpu_morph_batched_u16
+    _check(fn(src.data_ptr(), src.stride(1) * es, src.stride(0) * es, dst.data_ptr(), dst.stride(1) * es,
+              dst.stride(0) * es, b, w, h, wx, wy, op, border, value, _stream_ptr(stream)))
+
+
+def morph_band_device(src_with_halo, rows_above: int, rows_below: int, dst, wx, wy, op, border=REPLICATE,
+                      value=0, stream=None) -> None:
+    """``src_with_halo`` holds rows_above + band_rows + rows_below rows; dst holds band_rows."""
+    _dev(src_with_halo), _dev(dst)
+    rows, w = dst.shape
+    es = dst.element_size()
+    base = src_with_halo.data_ptr() + rows_above * src_with_halo.stride(0) * es
+    fn = lib().rmgpu_morph_band_u8 if es == 1 else lib().rmgpu_morph_band_u16
+    _check(fn(base, src_with_halo.stride(0) * es, dst.data_ptr(), dst.stride(0) * es, w, rows, rows_above,
+              rows_below, wx, wy, op, border, value, _stream_ptr(stream)))
+
+
+def transpose_device(src, dst, stream=None) -> None:
+    _dev(src), _dev(dst)
+    h, w = src.shape
+    es = src.element_size()
+    fn = lib().rmgpu_transpose_u8 if es == 1 else lib().rmgpu_transpose_u16
+    _check(fn(src.data_ptr(), src.stride(0) * es, dst.data_ptr(), dst.stride(0) * es, w, h, _stream_ptr(stream)))
+
+
+def transpose_tiles_device(data, n: int, n_tiles: int | None = None, row_stride: int | None = None,
+                           tile_step: int | None = None, stream=None) -> None:
+    import torch
+    es = data.element_size()
+    n_tiles = data.numel() // (n * n) if n_tiles is None else n_tiles
+    fn = {1: lib().rmgpu_transpose_tiles_u8, 2: lib().rmgpu_transpose_tiles_u16,
+          4: lib().rmgpu_transpose_tiles_u32}[es]
+    _check(fn(data.data_ptr(), n_tiles, n, n if row_stride is None else row_stride,
+              n * n if tile_step is None else tile_step, _stream_ptr(stream)))
+
+
+def generate_device(dst, seed: int, stream_id: int = 0, stream=None) -> None:
+    _dev(dst)
+    h, w = dst.shape
+    es = dst.element_size()
+    fn = lib().rmgpu_generate_u8 if es == 1 else lib().rmgpu_generate_u16
+    _check(fn(dst.data_ptr(), dst.stride(0) * es, w, h, seed, stream_id, _stream_ptr(stream)))
+
+
+def launch_count() -> int:
+    return int(lib().rmgpu_launch_count())
+
+
+def plan_name(elem_bytes: int, w: int, h: int, wx: int, wy: int, op: int = ERODE) -> str:
+    return lib().rmgpu_plan_name(elem_bytes, w, h, wx, wy, op).decode()

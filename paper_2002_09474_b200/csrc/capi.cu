@@ -1,0 +1,523 @@
+// capi.cu -- the extern "C" boundary declared in include/rmgpu.h.
+//
+// Validation mirrors the reference before any work is done (make_se image.cpp:18-24,
+// validate_window sliding_extrema.cpp:9-14, check_tile_side transpose.cpp:7-10,
+// Image::Image image.cpp:26-31); then the planner picks a kernel. No CPU fallback exists: every
+// pixel of every result is produced by a kernel in this library.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/rmgpu.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rmgpu {
+std::atomic<unsigned long long> g_launch_count{0};
+}
+
+using rmgpu::MorphJob;
+
+namespace {
+
+thread_local std::string t_last_error;
+
+int fail(int status, const std::string& msg) {
+    t_last_error = msg;
+    return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    t_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? RMGPU_ERR_OUT_OF_MEMORY : RMGPU_ERR_CUDA;
+}
+
+#define RM_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// make_se (image.cpp:18-24): zero check on both extents first, then parity.
+int check_se(int wx, int wy) {
+    if (wx < 1 || wy < 1) return fail(RMGPU_ERR_ZERO_EXTENT, "structuring element extents must be >= 1");
+    if (wx % 2 == 0 || wy % 2 == 0) return fail(RMGPU_ERR_EVEN_EXTENT, "structuring element extents must be odd");
+    return RMGPU_OK;
+}
+
+int check_window(int w) {  // validate_window (sliding_extrema.cpp:9-14)
+    if (w < 1) return fail(RMGPU_ERR_ZERO_EXTENT, "window extent must be >= 1");
+    if (w % 2 == 0) return fail(RMGPU_ERR_EVEN_EXTENT, "window extent must be odd");
+    return RMGPU_OK;
+}
+
+int check_device() {
+    static std::once_flag once;
+    static int status = RMGPU_OK;
+    static std::string msg;
+    std::call_once(once, [] {
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n == 0) {
+            status = RMGPU_ERR_NO_DEVICE;
+            msg = std::string("no CUDA device: ") + cudaGetErrorString(e);
+            return;
+        }
+        cudaDeviceProp p{};
+        cudaGetDeviceProperties(&p, 0);
+        if (p.major != 10) {
+            status = RMGPU_ERR_NO_DEVICE;
+            msg = "librmgpu is built for sm_100a only; device 0 is sm_" + std::to_string(p.major) +
+                  std::to_string(p.minor);
+        }
+    });
+    if (status != RMGPU_OK) return fail(status, msg);
+    return RMGPU_OK;
+}
+
+int check_image(const void* src, size_t sp, const void* dst, size_t dp, int W, int H, int elem) {
+    if (W < 0 || H < 0) return fail(RMGPU_ERR_BAD_ARGUMENT, "image dimensions must be non-negative");
+    if (W == 0 || H == 0) return RMGPU_OK;
+    if (!src || !dst) return fail(RMGPU_ERR_BAD_ARGUMENT, "null image pointer");
+    if (sp < (size_t)W * elem || dp < (size_t)W * elem || sp % elem || dp % elem)
+        return fail(RMGPU_ERR_BAD_ARGUMENT, "pitch smaller than a row or not a multiple of the pixel size");
+    return RMGPU_OK;
+}
+
+int check_op_border(int op, int border, unsigned bval, int elem) {
+    if (op < RMGPU_ERODE || op > RMGPU_GRADIENT) return fail(RMGPU_ERR_BAD_ARGUMENT, "unknown morphology op");
+    if (border != RMGPU_BORDER_REPLICATE && border != RMGPU_BORDER_CONSTANT)
+        return fail(RMGPU_ERR_BAD_ARGUMENT, "unknown border mode");
+    if (border == RMGPU_BORDER_CONSTANT && bval > (elem == 1 ? 0xFFu : 0xFFFFu))
+        return fail(RMGPU_ERR_BAD_ARGUMENT, "constant border value out of pixel range");
+    return RMGPU_OK;
+}
+
+// One erode / dilate / gradient over the job's rows. Window-1 axes are a copy
+// (separable.cpp:66,88); a 1x1 gradient is all zeros.
+int run_single(MorphJob j) {
+    if (j.gx == 0 && j.gy == 0) {
+        for (int b = 0; b < j.batch; ++b) {
+            char* d = static_cast<char*>(j.dst) + (size_t)b * j.dimg;
+            const char* s = static_cast<const char*>(j.src) + (size_t)b * j.simg;
+            if (j.mode == rmgpu::MODE_GRAD) RM_CUDA(cudaMemset2DAsync(d, j.dp, 0, (size_t)j.W * j.elem, j.H, j.stream));
+            else RM_CUDA(cudaMemcpy2DAsync(d, j.dp, s, j.sp, (size_t)j.W * j.elem, j.H, cudaMemcpyDeviceToDevice, j.stream));
+        }
+        return RMGPU_OK;
+    }
+    cudaError_t e = cudaSuccess;
+    if (rmgpu::launch_fast(j, &e)) {
+        if (e != cudaSuccess) return cuda_fail(e, "fast morph kernel");
+        return RMGPU_OK;
+    }
+    if (rmgpu::generic_tile_fits(j)) {
+        e = rmgpu::launch_generic_tile(j);
+        if (e != cudaSuccess) return cuda_fail(e, "generic morph kernel");
+        return RMGPU_OK;
+    }
+    // Very large windows: two global 1-D passes through an intermediate buffer.
+    const size_t row_bytes = (size_t)j.W * j.elem;
+    const size_t tmp_pitch = (row_bytes + 255) & ~size_t(255);
+    const size_t tmp_img = tmp_pitch * (size_t)j.H;
+    const int nbuf = j.mode == rmgpu::MODE_GRAD ? 3 : 1;
+    void* tmp = nullptr;
+    RM_CUDA(cudaMallocAsync(&tmp, tmp_img * j.batch * nbuf, j.stream));
+    auto run_pair = [&](int mode, void* out, size_t out_pitch, size_t out_img) -> int {
+        MorphJob v = j;
+        v.mode = mode;
+        v.dst = tmp;
+        v.dp = tmp_pitch;
+        v.dimg = tmp_img;
+        e = rmgpu::launch_pass_cols(v);
+        if (e != cudaSuccess) return cuda_fail(e, "vertical pass");
+        MorphJob h = j;
+        h.mode = mode;
+        h.src = tmp;
+        h.sp = tmp_pitch;
+        h.simg = tmp_img;
+        h.above = h.below = 0;
+        h.dst = out;
+        h.dp = out_pitch;
+        h.dimg = out_img;
+        e = rmgpu::launch_pass_rows(h);
+        if (e != cudaSuccess) return cuda_fail(e, "horizontal pass");
+        return RMGPU_OK;
+    };
+    int rc;
+    if (j.mode != rmgpu::MODE_GRAD) {
+        rc = run_pair(j.mode, j.dst, j.dp, j.dimg);
+    } else {
+        char* hi = static_cast<char*>(tmp) + tmp_img * j.batch;
+        char* lo = hi + tmp_img * j.batch;
+        rc = run_pair(rmgpu::MODE_MAX, hi, tmp_pitch, tmp_img);
+        if (rc == RMGPU_OK) rc = run_pair(rmgpu::MODE_MIN, lo, tmp_pitch, tmp_img);
+        for (int b = 0; rc == RMGPU_OK && b < j.batch; ++b) {
+            e = rmgpu::launch_subtract(hi + b * tmp_img, tmp_pitch, lo + b * tmp_img, tmp_pitch,
+                                       static_cast<char*>(j.dst) + b * j.dimg, j.dp, j.W, j.H, j.elem, j.stream);
+            if (e != cudaSuccess) rc = cuda_fail(e, "subtract");
+        }
+    }
+    cudaError_t fe = cudaFreeAsync(tmp, j.stream);
+    if (rc == RMGPU_OK && fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
+    return rc;
+}
+
+// Full op (erode/dilate/open/close/gradient) over a whole image, batch or row band.
+int run_morph(const void* src, size_t sp, size_t simg, void* dst, size_t dp, size_t dimg, int batch, int W,
+              int H, int above, int below, int wx, int wy, int op, int border, unsigned bval, int elem,
+              cudaStream_t stream) {
+    int rc;
+    if ((rc = check_se(wx, wy))) return rc;
+    if ((rc = check_op_border(op, border, bval, elem))) return rc;
+    if ((rc = check_image(src, sp, dst, dp, W, H, elem))) return rc;
+    if (above < 0 || below < 0 || batch < 0) return fail(RMGPU_ERR_BAD_ARGUMENT, "negative halo or batch");
+    if (W == 0 || H == 0 || batch == 0) return RMGPU_OK;
+    if ((rc = check_device())) return rc;
+
+    MorphJob j;
+    j.src = src; j.sp = sp; j.dst = dst; j.dp = dp; j.W = W; j.H = H;
+    j.above = above; j.below = below;
+    // Wings past the valid extent change nothing (every valid tap is already inside the window and
+    // at least one tap is outside it), so clamp them to keep tiles bounded.
+    j.gx = std::min(wx / 2, W);
+    j.gy = std::min(wy / 2, H + above + below);
+    j.cmode = border; j.bval = bval; j.elem = elem; j.batch = batch; j.simg = simg; j.dimg = dimg;
+    j.stream = stream;
+
+    if (op == RMGPU_ERODE || op == RMGPU_DILATE || op == RMGPU_GRADIENT) {
+        j.mode = op == RMGPU_ERODE ? rmgpu::MODE_MIN : op == RMGPU_DILATE ? rmgpu::MODE_MAX : rmgpu::MODE_GRAD;
+        return run_single(j);
+    }
+    // opening = dilate(erode(x)), closing = erode(dilate(x)) (dispatch.cpp:48-56): the first stage
+    // runs over the band plus up to one wing of halo rows, its result is a real image whose border
+    // (the true image border) is re-applied by the second stage.
+    const int ia = std::min(above, j.gy), ib = std::min(below, j.gy);
+    const int IH = H + ia + ib;
+    const size_t row_bytes = (size_t)W * elem;
+    const size_t tp = (row_bytes + 255) & ~size_t(255);
+    const size_t timg = tp * (size_t)IH;
+    void* tmp = nullptr;
+    RM_CUDA(cudaMallocAsync(&tmp, timg * batch, stream));
+    MorphJob a = j;
+    a.mode = op == RMGPU_OPEN ? rmgpu::MODE_MIN : rmgpu::MODE_MAX;
+    a.src = static_cast<const char*>(src) - (ptrdiff_t)ia * (ptrdiff_t)sp;
+    a.H = IH;
+    a.above = above - ia;
+    a.below = below - ib;
+    a.gy = std::min(wy / 2, IH + a.above + a.below);
+    a.dst = tmp; a.dp = tp; a.dimg = timg;
+    rc = run_single(a);
+    if (rc == RMGPU_OK) {
+        MorphJob b = j;
+        b.mode = op == RMGPU_OPEN ? rmgpu::MODE_MAX : rmgpu::MODE_MIN;
+        b.src = static_cast<const char*>(tmp) + (size_t)ia * tp;
+        b.sp = tp; b.simg = timg;
+        b.above = ia; b.below = ib;
+        b.gy = std::min(wy / 2, H + ia + ib);
+        rc = run_single(b);
+    }
+    cudaError_t fe = cudaFreeAsync(tmp, stream);
+    if (rc == RMGPU_OK && fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
+    return rc;
+}
+
+// Internal per-thread stream + cached pool for the synchronous host entry points.
+struct HostCtx {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+};
+thread_local HostCtx t_ctx;
+
+int host_stream(cudaStream_t* out) {
+    int rc = check_device();
+    if (rc) return rc;
+    int dev = 0;
+    RM_CUDA(cudaGetDevice(&dev));
+    if (t_ctx.stream == nullptr || t_ctx.device != dev) {
+        RM_CUDA(cudaStreamCreateWithFlags(&t_ctx.stream, cudaStreamNonBlocking));
+        t_ctx.device = dev;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;  // keep freed blocks cached between calls
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+    *out = t_ctx.stream;
+    return RMGPU_OK;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    ~DevBuf() { if (p) cudaFreeAsync(p, s); }
+};
+
+int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int wx, int wy, int op,
+               int border, unsigned bval, int elem) {
+    int rc;
+    if ((rc = check_se(wx, wy))) return rc;
+    if ((rc = check_op_border(op, border, bval, elem))) return rc;
+    if ((rc = check_image(hsrc, sp, hdst, dp, W, H, elem))) return rc;
+    if (W == 0 || H == 0) return RMGPU_OK;
+    cudaStream_t s;
+    if ((rc = host_stream(&s))) return rc;
+    const size_t rb = (size_t)W * elem, pitch = (rb + 255) & ~size_t(255);
+    DevBuf a, b;
+    a.s = b.s = s;
+    RM_CUDA(cudaMallocAsync(&a.p, pitch * H, s));
+    RM_CUDA(cudaMallocAsync(&b.p, pitch * H, s));
+    RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, rb, H, cudaMemcpyHostToDevice, s));
+    rc = run_morph(a.p, pitch, 0, b.p, pitch, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, elem, s);
+    if (rc) return rc;
+    RM_CUDA(cudaMemcpy2DAsync(hdst, dp, b.p, pitch, rb, H, cudaMemcpyDeviceToHost, s));
+    RM_CUDA(cudaStreamSynchronize(s));
+    return RMGPU_OK;
+}
+
+int pass_impl(int which, const void* src, size_t sp, void* dst, size_t dp, int W, int H, int window, int op,
+              int border, unsigned bval, cudaStream_t s) {
+    int rc;
+    if ((rc = check_window(window))) return rc;
+    if (which < RMGPU_PASS_HORIZONTAL || which > RMGPU_PASS_VERTICAL_VIA_TRANSPOSE)
+        return fail(RMGPU_ERR_BAD_ARGUMENT, "unknown pass");
+    if (op != RMGPU_ERODE && op != RMGPU_DILATE) return fail(RMGPU_ERR_BAD_ARGUMENT, "pass op must be erode or dilate");
+    const int wx = which == RMGPU_PASS_HORIZONTAL ? window : 1;
+    const int wy = which == RMGPU_PASS_HORIZONTAL ? 1 : window;
+    return run_morph(src, sp, 0, dst, dp, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, 1, s);
+}
+
+}  // namespace
+
+// =================================================================================================
+extern "C" {
+
+int rmgpu_abi_version(void) { return RMGPU_ABI_VERSION; }
+
+const char* rmgpu_last_error(void) { return t_last_error.c_str(); }
+
+const char* rmgpu_status_string(int status) {
+    switch (status) {
+    case RMGPU_OK: return "ok";
+    case RMGPU_ERR_ZERO_EXTENT: return "ZeroExtent";
+    case RMGPU_ERR_EVEN_EXTENT: return "EvenExtent";
+    case RMGPU_ERR_UNSUPPORTED_TILE: return "UnsupportedTile";
+    case RMGPU_ERR_BAD_CONFIG: return "BadConfig";
+    case RMGPU_ERR_BAD_ARGUMENT: return "BadArgument";
+    case RMGPU_ERR_CUDA: return "CudaError";
+    case RMGPU_ERR_NO_DEVICE: return "NoDevice";
+    case RMGPU_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+    default: return "unknown";
+    }
+}
+
+unsigned long long rmgpu_launch_count(void) { return rmgpu::g_launch_count.load(); }
+
+int rmgpu_resolve(int algo, int window, int axis, int threshold_h, int threshold_v) {
+    if (algo != RMGPU_ALGO_AUTO) return algo;  // dispatch.cpp:14-20
+    const int t = axis == RMGPU_AXIS_HORIZONTAL ? threshold_h : threshold_v;
+    return window <= t ? RMGPU_ALGO_LINEAR : RMGPU_ALGO_VANHERK;
+}
+
+const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int wy, int op) {
+    MorphJob j;
+    j.W = width; j.H = height; j.elem = elem_bytes;
+    j.gx = std::min(wx / 2, width);
+    j.gy = std::min(wy / 2, height);
+    j.mode = op == RMGPU_ERODE ? rmgpu::MODE_MIN : op == RMGPU_DILATE ? rmgpu::MODE_MAX : rmgpu::MODE_GRAD;
+    if (op == RMGPU_OPEN || op == RMGPU_CLOSE) j.mode = rmgpu::MODE_MIN;
+    if (j.gx == 0 && j.gy == 0) return "copy";
+    if (const char* n = rmgpu::fast_plan_name(j)) return n;
+    if (rmgpu::generic_tile_fits(j)) return "generic_tile";
+    return "two_pass_global";
+}
+
+#define MORPH_ENTRY(SFX, ELEM)                                                                          \
+    int rmgpu_morph_##SFX(const void* src, size_t sp, void* dst, size_t dp, int W, int H, int wx, int wy,   \
+                          int op, int border, unsigned bval, int algo_h, int algo_v, void* stream) {     \
+        (void)algo_h; (void)algo_v;                                                                       \
+        return run_morph(src, sp, 0, dst, dp, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, ELEM,           \
+                         (cudaStream_t)stream);                                                           \
+    }                                                                                                     \
+    int rmgpu_morph_batched_##SFX(const void* src, size_t sp, size_t simg, void* dst, size_t dp,          \
+                                  size_t dimg, int batch, int W, int H, int wx, int wy, int op,           \
+                                  int border, unsigned bval, void* stream) {                              \
+        return run_morph(src, sp, simg, dst, dp, dimg, batch, W, H, 0, 0, wx, wy, op, border, bval, ELEM, \
+                         (cudaStream_t)stream);                                                           \
+    }                                                                                                     \
+    int rmgpu_morph_band_##SFX(const void* src, size_t sp, void* dst, size_t dp, int W, int rows,         \
+                               int above, int below, int wx, int wy, int op, int border, unsigned bval,   \
+                               void* stream) {                                                            \
+        return run_morph(src, sp, 0, dst, dp, 0, 1, W, rows, above, below, wx, wy, op, border, bval,      \
+                         ELEM, (cudaStream_t)stream);                                                     \
+    }                                                                                                     \
+    int rmgpu_morph_host_##SFX(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int wx,  \
+                               int wy, int op, int border, unsigned bval, int algo_h, int algo_v) {       \
+        (void)algo_h; (void)algo_v;                                                                       \
+        return host_morph(hsrc, sp, hdst, dp, W, H, wx, wy, op, border, bval, ELEM);                      \
+    }
+
+MORPH_ENTRY(u8, 1)
+MORPH_ENTRY(u16, 2)
+
+int rmgpu_pass_u8(int which, const void* src, size_t sp, void* dst, size_t dp, int W, int H, int window,
+                  int op, int border, unsigned bval, int algo, void* stream) {
+    (void)algo;
+    return pass_impl(which, src, sp, dst, dp, W, H, window, op, border, bval, (cudaStream_t)stream);
+}
+
+int rmgpu_window_1d_u8(const void* in, size_t n, int window, int op, int border, unsigned bval, int algo,
+                       void* out, void* stream) {
+    (void)algo;
+    int rc;
+    if ((rc = check_window(window))) return rc;
+    if (n == 0) return RMGPU_OK;
+    if (n > 0x7fffffff) return fail(RMGPU_ERR_BAD_ARGUMENT, "1-D signal too long");
+    if (in != out)
+        return pass_impl(RMGPU_PASS_HORIZONTAL, in, n, out, n, (int)n, 1, window, op, border, bval,
+                         (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    void* tmp = nullptr;
+    RM_CUDA(cudaMallocAsync(&tmp, n, s));
+    RM_CUDA(cudaMemcpyAsync(tmp, in, n, cudaMemcpyDeviceToDevice, s));
+    rc = pass_impl(RMGPU_PASS_HORIZONTAL, tmp, n, out, n, (int)n, 1, window, op, border, bval, s);
+    cudaFreeAsync(tmp, s);
+    return rc;
+}
+
+int rmgpu_transpose_u8(const void* src, size_t sp, void* dst, size_t dp, int W, int H, void* stream) {
+    int rc;
+    if (W < 0 || H < 0) return fail(RMGPU_ERR_BAD_ARGUMENT, "image dimensions must be non-negative");
+    if (W == 0 || H == 0) return RMGPU_OK;
+    if (!src || !dst || sp < (size_t)W || dp < (size_t)H) return fail(RMGPU_ERR_BAD_ARGUMENT, "bad transpose buffers");
+    if ((rc = check_device())) return rc;
+    cudaError_t e = rmgpu::launch_transpose(src, sp, dst, dp, W, H, 1, (cudaStream_t)stream);
+    return e == cudaSuccess ? RMGPU_OK : cuda_fail(e, "transpose");
+}
+
+int rmgpu_transpose_u16(const void* src, size_t sp, void* dst, size_t dp, int W, int H, void* stream) {
+    int rc;
+    if (W < 0 || H < 0) return fail(RMGPU_ERR_BAD_ARGUMENT, "image dimensions must be non-negative");
+    if (W == 0 || H == 0) return RMGPU_OK;
+    if (!src || !dst || sp < 2 * (size_t)W || dp < 2 * (size_t)H || (sp | dp) & 1)
+        return fail(RMGPU_ERR_BAD_ARGUMENT, "bad transpose buffers");
+    if ((rc = check_device())) return rc;
+    cudaError_t e = rmgpu::launch_transpose(src, sp, dst, dp, W, H, 2, (cudaStream_t)stream);
+    return e == cudaSuccess ? RMGPU_OK : cuda_fail(e, "transpose");
+}
+
+static int tiles_impl(void* data, size_t n_tiles, int n, size_t rs, size_t step, int elem, void* stream) {
+    int rc;
+    if (n != 4 && n != 8 && n != 16) return fail(RMGPU_ERR_UNSUPPORTED_TILE, "tile side must be 4, 8 or 16");
+    if (n_tiles == 0) return RMGPU_OK;
+    if (!data || rs < (size_t)n) return fail(RMGPU_ERR_BAD_ARGUMENT, "bad tile buffer");
+    if ((rc = check_device())) return rc;
+    cudaError_t e = rmgpu::launch_transpose_tiles(data, n_tiles, n, rs, step, elem, (cudaStream_t)stream);
+    return e == cudaSuccess ? RMGPU_OK : cuda_fail(e, "transpose_tiles");
+}
+
+int rmgpu_transpose_tiles_u8(void* d, size_t nt, int n, size_t rs, size_t step, void* s) { return tiles_impl(d, nt, n, rs, step, 1, s); }
+int rmgpu_transpose_tiles_u16(void* d, size_t nt, int n, size_t rs, size_t step, void* s) { return tiles_impl(d, nt, n, rs, step, 2, s); }
+int rmgpu_transpose_tiles_u32(void* d, size_t nt, int n, size_t rs, size_t step, void* s) { return tiles_impl(d, nt, n, rs, step, 4, s); }
+
+static int transpose_host(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int elem) {
+    int rc;
+    if (W < 0 || H < 0) return fail(RMGPU_ERR_BAD_ARGUMENT, "image dimensions must be non-negative");
+    if (W == 0 || H == 0) return RMGPU_OK;
+    if (!hsrc || !hdst || sp < (size_t)W * elem || dp < (size_t)H * elem)
+        return fail(RMGPU_ERR_BAD_ARGUMENT, "bad transpose buffers");
+    cudaStream_t s;
+    if ((rc = host_stream(&s))) return rc;
+    const size_t pa = ((size_t)W * elem + 255) & ~size_t(255), pb = ((size_t)H * elem + 255) & ~size_t(255);
+    DevBuf a, b;
+    a.s = b.s = s;
+    RM_CUDA(cudaMallocAsync(&a.p, pa * H, s));
+    RM_CUDA(cudaMallocAsync(&b.p, pb * W, s));
+    RM_CUDA(cudaMemcpy2DAsync(a.p, pa, hsrc, sp, (size_t)W * elem, H, cudaMemcpyHostToDevice, s));
+    cudaError_t e = rmgpu::launch_transpose(a.p, pa, b.p, pb, W, H, elem, s);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose");
+    RM_CUDA(cudaMemcpy2DAsync(hdst, dp, b.p, pb, (size_t)H * elem, W, cudaMemcpyDeviceToHost, s));
+    RM_CUDA(cudaStreamSynchronize(s));
+    return RMGPU_OK;
+}
+
+int rmgpu_transpose_host_u8(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H) {
+    return transpose_host(hsrc, sp, hdst, dp, W, H, 1);
+}
+
+int rmgpu_transpose_host_u16(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H) {
+    return transpose_host(hsrc, sp, hdst, dp, W, H, 2);
+}
+
+int rmgpu_transpose_tiles_host(void* hdata, int elem, size_t n_tiles, int n, size_t rs, size_t step) {
+    int rc;
+    if (n != 4 && n != 8 && n != 16) return fail(RMGPU_ERR_UNSUPPORTED_TILE, "tile side must be 4, 8 or 16");
+    if (elem != 1 && elem != 2 && elem != 4) return fail(RMGPU_ERR_BAD_ARGUMENT, "element size must be 1, 2 or 4");
+    if (n_tiles == 0) return RMGPU_OK;
+    if (rs < (size_t)n) return fail(RMGPU_ERR_BAD_ARGUMENT, "bad tile stride");
+    cudaStream_t s;
+    if ((rc = host_stream(&s))) return rc;
+    const size_t span = ((n_tiles - 1) * step + (size_t)(n - 1) * rs + n) * elem;
+    DevBuf a;
+    a.s = s;
+    RM_CUDA(cudaMallocAsync(&a.p, span, s));
+    RM_CUDA(cudaMemcpyAsync(a.p, hdata, span, cudaMemcpyHostToDevice, s));
+    if ((rc = tiles_impl(a.p, n_tiles, n, rs, step, elem, s))) return rc;
+    RM_CUDA(cudaMemcpyAsync(hdata, a.p, span, cudaMemcpyDeviceToHost, s));
+    RM_CUDA(cudaStreamSynchronize(s));
+    return RMGPU_OK;
+}
+
+int rmgpu_pass_host_u8(int which, const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int window,
+                       int op, int border, unsigned bval, int algo) {
+    (void)algo;
+    int rc;
+    if ((rc = check_window(window))) return rc;
+    if ((rc = check_image(hsrc, sp, hdst, dp, W, H, 1))) return rc;
+    if (W == 0 || H == 0) return RMGPU_OK;
+    cudaStream_t s;
+    if ((rc = host_stream(&s))) return rc;
+    const size_t pitch = ((size_t)W + 255) & ~size_t(255);
+    DevBuf a, b;
+    a.s = b.s = s;
+    RM_CUDA(cudaMallocAsync(&a.p, pitch * H, s));
+    RM_CUDA(cudaMallocAsync(&b.p, pitch * H, s));
+    RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, W, H, cudaMemcpyHostToDevice, s));
+    if ((rc = pass_impl(which, a.p, pitch, b.p, pitch, W, H, window, op, border, bval, s))) return rc;
+    RM_CUDA(cudaMemcpy2DAsync(hdst, dp, b.p, pitch, W, H, cudaMemcpyDeviceToHost, s));
+    RM_CUDA(cudaStreamSynchronize(s));
+    return RMGPU_OK;
+}
+
+int rmgpu_window_1d_host_u8(const void* in, size_t n, int window, int op, int border, unsigned bval, int algo,
+                            void* out) {
+    (void)algo;
+    int rc;
+    if ((rc = check_window(window))) return rc;
+    if (n == 0) return RMGPU_OK;
+    if (n > 0x7fffffff) return fail(RMGPU_ERR_BAD_ARGUMENT, "1-D signal too long");
+    return rmgpu_pass_host_u8(RMGPU_PASS_HORIZONTAL, in, n, out, n, (int)n, 1, window, op, border, bval, algo);
+}
+
+int rmgpu_generate_u8(void* dst, size_t pitch, int W, int H, uint64_t seed, uint64_t sid, void* stream) {
+    int rc;
+    if (W < 0 || H < 0 || (W && H && (!dst || pitch < (size_t)W))) return fail(RMGPU_ERR_BAD_ARGUMENT, "bad generate args");
+    if ((rc = check_device())) return rc;
+    cudaError_t e = rmgpu::launch_generate(dst, pitch, W, H, seed, sid, 1, (cudaStream_t)stream);
+    return e == cudaSuccess ? RMGPU_OK : cuda_fail(e, "generate");
+}
+
+int rmgpu_generate_u16(void* dst, size_t pitch, int W, int H, uint64_t seed, uint64_t sid, void* stream) {
+    int rc;
+    if (W < 0 || H < 0 || (W && H && (!dst || pitch < 2 * (size_t)W || pitch & 1)))
+        return fail(RMGPU_ERR_BAD_ARGUMENT, "bad generate args");
+    if ((rc = check_device())) return rc;
+    cudaError_t e = rmgpu::launch_generate(dst, pitch, W, H, seed, sid, 2, (cudaStream_t)stream);
+    return e == cudaSuccess ? RMGPU_OK : cuda_fail(e, "generate");
+}
+
+}  // extern "C"

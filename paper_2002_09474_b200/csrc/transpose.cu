@@ -1,0 +1,206 @@
+// transpose.cu -- K4 whole-image transpose and K5 batched in-place tile transpose.
+//
+// K4 replaces rectmorph::transpose_image (core/src/transpose.cpp:29-53): out-of-place, dst is
+// H x W. A CTA moves one 64x64-element tile through shared memory: 16-byte coalesced loads of
+// input rows, column gathers out of shared memory, 16-byte coalesced stores of output rows.
+//
+// K5 replaces rectmorph::transpose_tile (transpose.cpp:14-27) batched over many tiles. The
+// reference transposes in place by log2(n) rounds of block interleaves
+// (transpose.hpp:19-30); on the GPU one thread owns a whole tile in registers and the same
+// permutation becomes (a) a 4x4-byte / 2x2-half transpose inside each group of words via PRMT
+// and (b) a compile-time renaming of the word groups. Tiles are contiguous (row stride n, tile
+// step n*n) on the fast path; any stride/step uses a shared-memory path.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rmgpu {
+
+namespace {
+
+// ------------------------------------------------------------------------------------------
+// K4: image transpose
+// ------------------------------------------------------------------------------------------
+constexpr int kTT = 64;  // tile side in elements
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+transpose_image_kernel(const T* __restrict__ src, size_t sp, T* __restrict__ dst, size_t dp, int W,
+                       int H, int vec_ok) {
+    constexpr int VE = 16 / sizeof(T);          // elements per 16-byte vector
+    constexpr int PITCH = kTT + VE;             // smem row pitch (elements), 16-B multiple
+    __shared__ __align__(16) T tile[kTT * PITCH];
+    const int x0 = blockIdx.x * kTT, y0 = blockIdx.y * kTT;
+    const int tid = threadIdx.x;
+    const bool full = vec_ok && (x0 + kTT <= W) && (y0 + kTT <= H);
+
+    // load 64 rows x 64 elements
+    constexpr int VPR = kTT / VE;               // vectors per tile row
+    if (full) {
+        for (int v = tid; v < kTT * VPR; v += 256) {
+            const int r = v / VPR, c = (v % VPR) * VE;
+            const uint4 val = *reinterpret_cast<const uint4*>(src + (size_t)(y0 + r) * sp + x0 + c);
+            *reinterpret_cast<uint4*>(tile + r * PITCH + c) = val;
+        }
+    } else {
+        for (int i = tid; i < kTT * kTT; i += 256) {
+            const int r = i / kTT, c = i % kTT;
+            if (y0 + r < H && x0 + c < W) tile[r * PITCH + c] = src[(size_t)(y0 + r) * sp + x0 + c];
+        }
+    }
+    __syncthreads();
+
+    // store: output row (x0 + c) holds input column c, rows y0 .. y0+63
+    if (full) {
+        // warp w: segment (w % VPR) of output rows; lanes = consecutive output rows (columns c)
+        for (int v = tid; v < kTT * VPR; v += 256) {
+            const int lane = v & 31, w = v >> 5;
+            const int seg = w % VPR, c = (w / VPR) * 32 + lane;
+            T vals[VE];
+#pragma unroll
+            for (int k = 0; k < VE; ++k) vals[k] = tile[(seg * VE + k) * PITCH + c];
+            *reinterpret_cast<uint4*>(dst + (size_t)(x0 + c) * dp + y0 + seg * VE) =
+                *reinterpret_cast<const uint4*>(vals);
+        }
+    } else {
+        for (int i = tid; i < kTT * kTT; i += 256) {
+            const int c = i / kTT, r = i % kTT;
+            if (y0 + r < H && x0 + c < W) dst[(size_t)(x0 + c) * dp + y0 + r] = tile[r * PITCH + c];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K5: batched tile transposes, one tile per thread (contiguous tiles)
+// ------------------------------------------------------------------------------------------
+// 4x4 byte transpose of four row words a[0..3] -> column words b[0..3].
+__device__ __forceinline__ void t4x4_u8(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t& b0, uint32_t& b1, uint32_t& b2, uint32_t& b3) {
+    const uint32_t t0 = prmt(a0, a1, 0x5140), t1 = prmt(a0, a1, 0x7362);
+    const uint32_t t2 = prmt(a2, a3, 0x5140), t3 = prmt(a2, a3, 0x7362);
+    b0 = prmt(t0, t2, 0x5410);
+    b1 = prmt(t0, t2, 0x7632);
+    b2 = prmt(t1, t3, 0x5410);
+    b3 = prmt(t1, t3, 0x7632);
+}
+
+// u8 tile of side N (4, 8, 16): N rows x N/4 words.
+template <int N>
+__global__ void __launch_bounds__(128)
+tiles_u8_kernel(uint8_t* __restrict__ data, size_t n_tiles) {
+    constexpr int WPR = N / 4;             // words per row
+    constexpr int NW = N * WPR;            // words per tile
+    constexpr int NV = NW / 4;             // uint4 per tile
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    uint4* p = reinterpret_cast<uint4*>(data + t * (size_t)(N * N));
+    uint32_t w[NW], o[NW];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const uint4 q = p[v];
+        w[4 * v + 0] = q.x; w[4 * v + 1] = q.y; w[4 * v + 2] = q.z; w[4 * v + 3] = q.w;
+    }
+    // word (r, k) = w[r*WPR + k] holds columns 4k..4k+3 of row r. Block (m, k) = rows 4m..4m+3
+    // of word column k transposes into output rows 4k..4k+3, word column m.
+#pragma unroll
+    for (int m = 0; m < WPR; ++m)
+#pragma unroll
+        for (int k = 0; k < WPR; ++k)
+            t4x4_u8(w[(4 * m + 0) * WPR + k], w[(4 * m + 1) * WPR + k], w[(4 * m + 2) * WPR + k],
+                    w[(4 * m + 3) * WPR + k], o[(4 * k + 0) * WPR + m], o[(4 * k + 1) * WPR + m],
+                    o[(4 * k + 2) * WPR + m], o[(4 * k + 3) * WPR + m]);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) p[v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+}
+
+// u16 tile of side N (4, 8): N rows x N/2 words; 2x2 half-word blocks.
+template <int N>
+__global__ void __launch_bounds__(128)
+tiles_u16_kernel(uint16_t* __restrict__ data, size_t n_tiles) {
+    constexpr int WPR = N / 2;
+    constexpr int NW = N * WPR;
+    constexpr int NV = NW / 4;
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    uint4* p = reinterpret_cast<uint4*>(data + t * (size_t)(N * N));
+    uint32_t w[NW], o[NW];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const uint4 q = p[v];
+        w[4 * v + 0] = q.x; w[4 * v + 1] = q.y; w[4 * v + 2] = q.z; w[4 * v + 3] = q.w;
+    }
+#pragma unroll
+    for (int m = 0; m < WPR; ++m)
+#pragma unroll
+        for (int k = 0; k < WPR; ++k) {
+            const uint32_t a = w[(2 * m) * WPR + k], b = w[(2 * m + 1) * WPR + k];
+            o[(2 * k) * WPR + m] = prmt(a, b, 0x5410);
+            o[(2 * k + 1) * WPR + m] = prmt(a, b, 0x7632);
+        }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) p[v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+}
+
+// Any element type, stride and step: one CTA per group of tiles through shared memory.
+template <typename T>
+__global__ void __launch_bounds__(256)
+tiles_generic_kernel(T* __restrict__ data, size_t n_tiles, int n, size_t row_stride, size_t step) {
+    __shared__ T buf[256];
+    const int per = 256 / (n * n);   // tiles per CTA pass
+    const int tid = threadIdx.x;
+    const int local = tid / (n * n), e = tid % (n * n);
+    const int r = e / n, c = e % n;
+    for (size_t base = (size_t)blockIdx.x * per; base < n_tiles; base += (size_t)gridDim.x * per) {
+        const size_t t = base + local;
+        const bool live = local < per && t < n_tiles;
+        if (live) buf[tid] = data[t * step + (size_t)r * row_stride + c];
+        __syncthreads();
+        if (live) data[t * step + (size_t)r * row_stride + c] = buf[local * n * n + c * n + r];
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_transpose(const void* src, size_t sp, void* dst, size_t dp, int W, int H, int elem,
+                             cudaStream_t s) {
+    dim3 grid(cdiv(W, kTT), cdiv(H, kTT));
+    const int vec_ok = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | sp | dp) & 15) == 0;
+    if (elem == 1)
+        transpose_image_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)src, sp, (uint8_t*)dst, dp, W, H, vec_ok);
+    else
+        transpose_image_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)src, sp / 2, (uint16_t*)dst,
+                                                              dp / 2, W, H, vec_ok);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_transpose_tiles(void* data, size_t n_tiles, int n, size_t row_stride, size_t tile_step,
+                                   int elem, cudaStream_t s) {
+    if (n_tiles == 0) return cudaSuccess;
+    const bool contiguous = row_stride == (size_t)n && tile_step == (size_t)n * n &&
+                            (reinterpret_cast<uintptr_t>(data) & 15) == 0;
+    const unsigned blocks = (unsigned)((n_tiles + 127) / 128);
+    if (contiguous && elem == 1) {
+        if (n == 4) tiles_u8_kernel<4><<<blocks, 128, 0, s>>>((uint8_t*)data, n_tiles);
+        else if (n == 8) tiles_u8_kernel<8><<<blocks, 128, 0, s>>>((uint8_t*)data, n_tiles);
+        else tiles_u8_kernel<16><<<blocks, 128, 0, s>>>((uint8_t*)data, n_tiles);
+        count_launch();
+        return cudaGetLastError();
+    }
+    if (contiguous && elem == 2 && n <= 8) {
+        if (n == 4) tiles_u16_kernel<4><<<blocks, 128, 0, s>>>((uint16_t*)data, n_tiles);
+        else tiles_u16_kernel<8><<<blocks, 128, 0, s>>>((uint16_t*)data, n_tiles);
+        count_launch();
+        return cudaGetLastError();
+    }
+    const size_t per = 256 / ((size_t)n * n);
+    const size_t want = (n_tiles + per - 1) / per;
+    const unsigned grid = (unsigned)(want < 148 * 64 ? want : 148 * 64);
+    if (elem == 1) tiles_generic_kernel<uint8_t><<<grid, 256, 0, s>>>((uint8_t*)data, n_tiles, n, row_stride, tile_step);
+    else if (elem == 2) tiles_generic_kernel<uint16_t><<<grid, 256, 0, s>>>((uint16_t*)data, n_tiles, n, row_stride, tile_step);
+    else tiles_generic_kernel<uint32_t><<<grid, 256, 0, s>>>((uint32_t*)data, n_tiles, n, row_stride, tile_step);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace rmgpu
