@@ -26,7 +26,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
                      "-I", os.path.join(ROOT, "include")]
-CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_fast.cu", "transpose.cu", "generate.cu"]
+CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_fast.cu", "morph_fast_u8_min.cu", "morph_fast_u8_max.cu",
+              "morph_fast_u16_min.cu", "morph_fast_u16_max.cu", "transpose.cu", "generate.cu"]
 HOST_SOURCES = [os.path.join("host", "rectmorph_b200.cpp")]
 
 
