@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -26,6 +27,11 @@ using rmgpu::MorphJob;
 namespace {
 
 thread_local std::string t_last_error;
+// Test hook: RMGPU_DISABLE_STREAM=1 routes around the streaming kernel (exercises the fallbacks).
+const bool g_disable_stream = [] {
+    const char* v = getenv("RMGPU_DISABLE_STREAM");
+    return v && v[0] == '1';
+}();
 
 int fail(int status, const std::string& msg) {
     t_last_error = msg;
@@ -111,6 +117,10 @@ int run_single(MorphJob j) {
         return RMGPU_OK;
     }
     cudaError_t e = cudaSuccess;
+    if (!g_disable_stream && rmgpu::stream::launch(j, &e)) {
+        if (e != cudaSuccess) return cuda_fail(e, "stream morph kernel");
+        return RMGPU_OK;
+    }
     if (rmgpu::launch_fast(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "fast morph kernel");
         return RMGPU_OK;
@@ -331,6 +341,8 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
     j.mode = op == RMGPU_ERODE ? rmgpu::MODE_MIN : op == RMGPU_DILATE ? rmgpu::MODE_MAX : rmgpu::MODE_GRAD;
     if (op == RMGPU_OPEN || op == RMGPU_CLOSE) j.mode = rmgpu::MODE_MIN;
     if (j.gx == 0 && j.gy == 0) return "copy";
+    if (!g_disable_stream)
+        if (const char* n = rmgpu::stream::plan_name(j)) return n;
     if (const char* n = rmgpu::fast_plan_name(j)) return n;
     if (rmgpu::generic_tile_fits(j)) return "generic_tile";
     return "two_pass_global";

@@ -41,6 +41,12 @@ cudaError_t launch_subtract(const void* a, size_t ap, const void* b, size_t bp, 
 bool launch_fast(const MorphJob& j, cudaError_t* err);
 const char* fast_plan_name(const MorphJob& j);
 
+// ---- strip-streaming fused path (morph_stream.cu), preferred over launch_fast ------------------
+namespace stream {
+bool launch(const MorphJob& j, cudaError_t* err);
+const char* plan_name(const MorphJob& j);
+}  // namespace stream
+
 // ---- transposes (transpose.cu) ---------------------------------------------------------------
 cudaError_t launch_transpose(const void* src, size_t sp, void* dst, size_t dp, int W, int H,
                              int elem, cudaStream_t s);

@@ -1,0 +1,10 @@
+// Instantiates the streaming kernel variants for u8 / min (split across files for parallel builds).
+#include "morph_stream.cuh"
+
+namespace rmgpu {
+namespace stream {
+cudaError_t dispatch_u8_min(const MorphJob& j, int vb, int hb, int rh, int B, int q) {
+    return stream_dispatch<uint8_t, MODE_MIN>(j, vb, hb, rh, B, q);
+}
+}  // namespace stream
+}  // namespace rmgpu
