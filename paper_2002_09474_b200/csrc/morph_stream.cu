@@ -43,7 +43,6 @@ bool choose(const MorphJob& j, Choice* c) {
     if (j.elem != 1 && j.elem != 2) return false;
     if ((reinterpret_cast<uintptr_t>(j.src) | j.sp | (j.batch > 1 ? j.simg : 0)) & 15) return false;
     const int tw = j.elem == 1 ? SG<uint8_t>::TW : SG<uint16_t>::TW;
-    if ((tw + 2 * j.gx + HC - 1) / HC > 64) return false;  // chunk-min scratch
     const int w1 = 2 * j.gy;
     if (j.gy <= 3) {
         c->vb = 2 * j.gy + 1;
@@ -66,13 +65,13 @@ bool choose(const MorphJob& j, Choice* c) {
         }
         if (!c->vb) return false;
     }
-    c->hb = j.gx <= 3 ? 2 * j.gx + 1 : HC;
-    const bool hblock = c->hb > 7;
-    const Plan pl = j.elem == 1 ? make_plan<uint8_t>(c->B, c->q, j.gx, hblock) : make_plan<uint16_t>(c->B, c->q, j.gx, hblock);
-    if (pl.total > 220 * 1024) return false;
-    c->smem = pl.total;
+    c->hb = j.gx <= 3 ? 2 * j.gx + 1 : (j.gx <= stream_gxmax(j.elem, 8) ? 8 : 9);
+    if (j.gx > stream_gxmax(j.elem, c->hb)) return false;
+    const int total = j.elem == 1 ? stream_smem<uint8_t>(c->hb, c->B, c->q) : stream_smem<uint16_t>(c->hb, c->B, c->q);
+    if (total > 220 * 1024) return false;
+    c->smem = total;
     // rows per CTA: enough CTAs for ~2 waves of the resident capacity, long runs for big windows
-    const int occ = std::max(1, std::min(8, (227 * 1024) / (pl.total + 1024)));
+    const int occ = std::max(1, std::min(8, (227 * 1024) / (total + 1024)));
     const long strips = (long)((j.W + tw - 1) / tw) * j.batch;
     const long target = 148L * occ * 2;
     long splits = std::max(1L, (target + strips - 1) / strips);

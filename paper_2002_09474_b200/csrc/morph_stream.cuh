@@ -8,9 +8,7 @@
 namespace rmgpu {
 namespace stream {
 
-constexpr int NVW = 4;                 // vertical warps
-constexpr int NHW = 4;                 // horizontal warps
-constexpr int NTH = 32 * (NVW + NHW);  // threads per CTA
+constexpr int NHW = 4;                 // horizontal warps (vertical warp count depends on the class)
 constexpr int PF = 2;                  // input blocks prefetched ahead of the leading block
 constexpr int QMAX = 6;                // whole blocks between suffix run and prefix block (registers)
 constexpr int VCH = 16;                // rows per iteration for the direct vertical variants
@@ -124,90 +122,90 @@ struct StreamParams {
     int rh;               // output rows per CTA
 };
 
-// Shared-memory plan, identical on host and device.
-struct Plan {
-    int B;        // rows per iteration (block size)
-    int NSB;      // ring slots (blocks)
-    int RP;       // ring row pitch (bytes)
-    int VTWE;     // transposed-tile row length (entries)
-    int NGC;      // row groups per chunk
-    int off_ring, off_vt, off_hs, off_out, total;
-    int HSE;      // per-warp horizontal scratch entries
+// Compile-time geometry of one horizontal class HB: 1/3/5/7 = direct window (gx = (HB-1)/2),
+// 8 / 9 = lane-chunk block algorithm for gx up to GXMAX (small / large halo).
+template <typename T, int HB>
+struct HG {
+    static constexpr int sz = sizeof(T);
+    static constexpr int TW = SG<T>::TW;
+    static constexpr int GXMAX = HB <= 7 ? (HB - 1) / 2 : (HB == 8 ? (sz == 1 ? 48 : 24) : (sz == 1 ? 112 : 56));
+    static constexpr int RP = ((TW * sz + 2 * GXMAX * sz + 31) / 16) * 16;  // ring row pitch (bytes)
+    static constexpr int NCH = (TW + 2 * GXMAX + 7) / 8 + 2;                // 8-column chunks (+ slack)
+    static constexpr int NCHP = NCH | 1;                                     // odd: conflict-free lanes
+    static constexpr int VTG = 8 * NCHP;                                     // entries per row group
+    static constexpr int LPG = TW / 8;                                       // lanes per row group
+    static constexpr int NVW = (RP / (2 * sz) + 31) / 32;                    // vertical warps (2 px/thread)
+    static constexpr int NTH = 32 * (NVW + NHW);                             // threads per CTA
 };
 
-template <typename T>
-__host__ __device__ inline Plan make_plan(int B, int q, int gx, bool hblock) {
+// Shared-memory plan, identical on host and device (B and q runtime -> NSB; rest compile-time).
+struct Plan {
+    int NSB, off_ring, off_vt, off_hs, off_out, total;
+};
+
+template <typename T, int HB>
+__host__ __device__ inline Plan make_plan(int B, int q) {
+    using H = HG<T, HB>;
     using G = SG<T>;
     Plan p;
-    p.B = B;
     p.NSB = q + 2 + PF;
-    const int sz = (int)sizeof(T);
-    p.RP = ((G::TW * sz + 2 * gx * sz + 31) / 16) * 16;
-    const int cols = p.RP / sz;
-    p.VTWE = ((cols + HC + 16 + G::SWB - 1) / G::SWB) * G::SWB;  // slack: last lane chunk may overrun
-    p.NGC = B / G::GR;
-    p.HSE = hblock ? ((G::TW + 2 * gx + HC + G::SWB - 1) / G::SWB) * G::SWB : 0;
     int o = 64 * 8;  // mbarriers
     p.off_ring = o;
-    o += p.NSB * B * p.RP;
+    o += p.NSB * B * H::RP;
     p.off_vt = o;
-    o += 2 * p.NGC * p.VTWE * G::ESZ;
+    o += 2 * (B / G::GR) * H::VTG * G::ESZ;
     p.off_hs = o;
-    o += hblock ? NHW * (p.HSE + 64) * G::ESZ : 0;
+    if (HB > 7) o += NHW * (32 / H::LPG) * (H::VTG + H::NCHP) * G::ESZ;
     p.off_out = o;
-    o += B * (G::TW * sz + 16);
+    o += B * (G::TW * (int)sizeof(T) + 16);
     p.total = o;
     return p;
 }
 
+// Column fix-up for a 2-pixel word at image column c: byte source nibbles over (raw, Z), where Z
+// bytes 0 (and 1 for u16) hold the constant border value. Returns the ring byte offset to load.
 template <typename T>
-__device__ __forceinline__ int swz(int e) {
-    constexpr int S = SG<T>::SWB;
-    return (e & ~(S - 1)) | ((e & (S - 1)) ^ ((e / S) & (S - 1)));
-}
-
-// Column fix-up for a word at image column c: returns ring byte offset to load (relative to
-// the strip's first byte xs_b) and a PRMT selector over (raw, bword).
-template <typename T>
-__device__ __forceinline__ void col_fix(int c, int W, int cmode, int xs_col, int& load_off, uint32_t& sel, bool& fix) {
-    constexpr int PX = SG<T>::PX;
+__device__ __forceinline__ void col_fix(int c, int W, int cmode, int xs_col, int& load_off, uint32_t& nib,
+                                        bool& fix) {
     constexpr int sz = sizeof(T);
-    if (c >= 0 && c + PX - 1 < W) {
-        load_off = (c - xs_col) * sz;
-        sel = 0x3210;
-        fix = false;
-        return;
-    }
-    fix = true;
+    fix = !(c >= 0 && c + 1 < W);
     const int cc0 = min(max(c, 0), W - 1);
-    const int cl = (cc0 / PX) * PX;
+    const int cl = fix ? (cc0 / 2) * 2 : c;
     load_off = (cl - xs_col) * sz;
-    sel = 0;
+    nib = 0;
 #pragma unroll
-    for (int j = 0; j < PX; ++j) {
+    for (int j = 0; j < 2; ++j) {
         const int col = c + j;
 #pragma unroll
         for (int b = 0; b < sz; ++b) {
-            int nib;
-            if (cmode && (col < 0 || col >= W)) nib = 4 + b;
-            else nib = (min(max(col, 0), W - 1) - cl) * sz + b;
-            sel |= (uint32_t)nib << (4 * (j * sz + b));
+            int n;
+            if (!fix) n = j * sz + b;
+            else if (cmode && (col < 0 || col >= W)) n = 4 + b;
+            else n = (min(max(col, 0), W - 1) - cl) * sz + b;
+            nib |= (uint32_t)n << (4 * (j * sz + b));
         }
     }
 }
 
+__device__ __forceinline__ uint32_t nib_at(uint32_t nib, int k) { return (nib >> (4 * k)) & 0xF; }
+
 // ---- the kernel ------------------------------------------------------------------------------
-// VB: vertical variant: 1/3/5/7 = direct window (VCH rows per iteration), 8/16/24 = block size.
-// HB: horizontal variant: 1/3/5/7 = direct window, 8 = lane-chunk block algorithm (HC = 8).
+// VB: vertical variant: 1/3/5/7 = direct window (VCH rows per iteration), 8/16/24 = block size B.
+// HB: horizontal class (HG).
 template <typename T, int MODE, int VB, int HB>
-__global__ void __launch_bounds__(NTH)
+__global__ void __launch_bounds__(HG<T, HB>::NTH)
 morph_stream_kernel(StreamParams p) {
     using G = SG<T>;
+    using H = HG<T, HB>;
     constexpr int PX = G::PX, GR = G::GR, TW = G::TW, ESZ = G::ESZ;
     constexpr int sz = sizeof(T);
     constexpr bool VDIRECT = VB <= 7;
     constexpr int B = VDIRECT ? VCH : VB;
+    constexpr int NGC = B / GR;          // row groups per chunk
     constexpr int OUTP = TW * sz + 16;
+    constexpr int RP = H::RP, NCHP = H::NCHP, VTG = H::VTG, LPG = H::LPG;
+    constexpr int NVW = H::NVW, NTH = H::NTH;
+    constexpr int SUBG = 32 / LPG;       // row groups per warp pass
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int gx = p.gx, gy = p.gy;
@@ -215,7 +213,8 @@ morph_stream_kernel(StreamParams p) {
     const int q = VDIRECT ? 0 : w1 / B;
     const int r = VDIRECT ? w1 : w1 - q * B;
     const int s = r & 3;
-    const Plan pl = make_plan<T>(B, q, gx, HB > 7);
+    const Plan pl = make_plan<T, HB>(B, q);
+    const int NSB = pl.NSB;
 
     const uint8_t* src = p.src + blockIdx.z * p.simg;
     uint8_t* dst = p.dst + blockIdx.z * p.dimg;
@@ -229,10 +228,10 @@ morph_stream_kernel(StreamParams p) {
     const int xe_b = ((x0 + TW + gx) * sz + 15) / 16 * 16;
     const int w_b16 = (p.W * sz + 15) / 16 * 16;
     const int cb0 = max(xs_b, 0);
-    const int cb1 = min(xe_b, w_b16);
-    const int copy_len = cb1 - cb0;  // bytes copied per row (multiple of 16, > 0)
-    const int nwv = (xe_b - xs_b) / 4;
-    const int y_first = y0 - gy;     // image row of input index 0
+    const int copy_len = min(xe_b, w_b16) - cb0;  // bytes copied per row (multiple of 16)
+    const int nwv = (xe_b - xs_b) / (2 * sz);     // 2-pixel column words
+    const int off = (x0 - gx) - xs_col;           // horizontal input position 0 = strip column off
+    const int y_first = y0 - gy;                  // image row of input index 0
     const int Lend = (rh - 1 + w1 - s) / B;
     int Lf = 0;
     while (s + Lf * B - w1 + B - 1 < 0) ++Lf;
@@ -243,13 +242,11 @@ morph_stream_kernel(StreamParams p) {
     unsigned char* hs = smem + pl.off_hs;
     unsigned char* outt = smem + pl.off_out;
 
-    uint32_t bword = p.bval & 0xFF;
-    if constexpr (sz == 1) bword *= 0x01010101u;
-    else bword = (p.bval & 0xFFFF) * 0x00010001u;
+    const uint32_t bv = sz == 1 ? (p.bval & 0xFF) : (p.bval & 0xFFFF);
 
     const int tid = threadIdx.x;
     if (tid == 0) {
-        for (int k = 0; k < pl.NSB; ++k) mbar_init(&full[k], 1);
+        for (int k = 0; k < NSB; ++k) mbar_init(&full[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -258,147 +255,157 @@ morph_stream_kernel(StreamParams p) {
 
     if (warp < NVW) {
         // ================= vertical role: producer (warp 0) + streaming column sweeps =========
-        const int t = tid;  // column word
+        // thread t owns image columns xs_col + 2t, +1 as one u16x2 word (u8 unpacked on load)
+        const int t = tid;
         const bool active = t < nwv;
         int load_off = 0;
-        uint32_t sel = 0x3210;
+        uint32_t nib = 0;
         bool fix = false;
-        if (active) col_fix<T>(xs_col + PX * t, p.W, p.cmode, xs_col, load_off, sel, fix);
+        col_fix<T>(xs_col + 2 * (active ? t : 0), p.W, p.cmode, xs_col, load_off, nib, fix);
+        // u8: unpack + border fix in one PRMT over (raw16, Z), Z = {bval, 0, 0, 0}
+        const uint32_t selU = sz == 1 ? ((nib & 0xF) | (5u << 4) | (((nib >> 4) & 0xF) << 8) | (5u << 12)) : nib;
+        const uint32_t Z = bv;  // u16: bytes {lo, hi, 0, 0} -> nibbles 4, 5
+
+        // VT destinations of this thread's 2 columns (position = column - off), -1 = unused
+        int voff0, voff1;
+        {
+            const int pos0 = 2 * t - off, pos1 = pos0 + 1;
+            voff0 = (active && pos0 >= 0 && pos0 < 8 * H::NCH) ? ((pos0 & 7) * NCHP + (pos0 >> 3)) * ESZ : -1;
+            voff1 = (active && pos1 >= 0 && pos1 < 8 * H::NCH) ? ((pos1 & 7) * NCHP + (pos1 >> 3)) * ESZ : -1;
+        }
 
         // issue block k (rows [s + kB, s + kB + B) of the input index space) into its slot
         auto issue = [&](int k) {
-            const int slot = (k + 1) % pl.NSB;
-            unsigned char* base = ring + (size_t)slot * B * pl.RP;
-            uint32_t bytes = 0;
-            if (lane == 0) {
-                for (int m = 0; m < B; ++m) {
-                    const int y = y_first + s + k * B + m;
-                    if (!(p.cmode && (y < p.row_lo || y >= p.row_hi))) bytes += copy_len;
-                }
-            }
-            // constant rows outside the image: the warp fills them with the border value
-            for (int m = 0; m < B; ++m) {
-                const int y = y_first + s + k * B + m;
-                if (p.cmode && (y < p.row_lo || y >= p.row_hi)) {
-                    uint4* row = reinterpret_cast<uint4*>(base + (size_t)m * pl.RP);
-                    for (int c = lane; c < pl.RP / 16; c += 32) row[c] = make_uint4(bword, bword, bword, bword);
-                }
+            const int slot = (k + 1) % NSB;
+            unsigned char* base = ring + (size_t)slot * B * RP;
+            const int y = y_first + s + k * B + lane;
+            const bool inrow = lane < B;
+            const bool outside = p.cmode && (y < p.row_lo || y >= p.row_hi);
+            const unsigned cp = __ballot_sync(0xffffffffu, inrow && !outside);
+            unsigned fillm = __ballot_sync(0xffffffffu, inrow && outside);
+            while (fillm) {  // constant rows outside the image: the warp writes the border value
+                const int m = __ffs(fillm) - 1;
+                fillm &= fillm - 1;
+                const uint32_t bw = sz == 1 ? bv * 0x01010101u : bv * 0x00010001u;
+                uint4* row = reinterpret_cast<uint4*>(base + (size_t)m * RP);
+                for (int c = lane; c < RP / 16; c += 32) row[c] = make_uint4(bw, bw, bw, bw);
             }
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive_tx(&full[slot], bytes);
-                for (int m = 0; m < B; ++m) {
-                    const int y = y_first + s + k * B + m;
-                    if (p.cmode && (y < p.row_lo || y >= p.row_hi)) continue;
-                    const int yc = min(max(y, p.row_lo), p.row_hi - 1);
-                    bulk_g2s(base + (size_t)m * pl.RP + (cb0 - xs_b), src + (ptrdiff_t)yc * (ptrdiff_t)p.sp + cb0,
-                             (uint32_t)copy_len, &full[slot]);
-                }
+            if (lane == 0) mbar_arrive_tx(&full[slot], (uint32_t)(__popc(cp) * copy_len));
+            __syncwarp();
+            if (inrow && !outside) {
+                const int yc = min(max(y, p.row_lo), p.row_hi - 1);
+                bulk_g2s(base + (size_t)lane * RP + (cb0 - xs_b), src + (ptrdiff_t)yc * (ptrdiff_t)p.sp + cb0,
+                         (uint32_t)copy_len, &full[slot]);
             }
         };
         if (warp == 0) {
             for (int k = -1; k < PF && k <= Lend; ++k) issue(k);
         }
 
-        auto slot_base = [&](int k) -> const unsigned char* {
-            return ring + (size_t)((k + 1) % pl.NSB) * B * pl.RP + load_off;
+        auto ldw = [&](const unsigned char* a) -> uint32_t {
+            if constexpr (sz == 1) {
+                const uint32_t raw = *reinterpret_cast<const uint16_t*>(a);
+                return prmt(raw, Z, selU);
+            } else {
+                const uint32_t raw = *reinterpret_cast<const uint32_t*>(a);
+                return fix ? prmt(raw, Z, selU) : raw;
+            }
         };
-        auto ldw = [&](const unsigned char* a) -> LW<T> {
-            uint32_t raw = *reinterpret_cast<const uint32_t*>(a);
-            if (fix) raw = prmt(raw, bword, sel);
-            return unpack_w(raw, (T*)nullptr);
-        };
+        auto op2 = [](uint32_t x, uint32_t y) { return red2_u16x2<MODE>(x, y); };
+        auto op3 = [](uint32_t x, uint32_t y, uint32_t z) { return red3_u16x2<MODE>(x, y, z); };
+        constexpr uint32_t IDV = MODE == MODE_MIN ? 0xFFFFFFFFu : 0u;
 
-        LW<T> M[QMAX];
+        uint32_t M[QMAX];
 #pragma unroll
-        for (int k = 0; k < QMAX; ++k) M[k] = lid<T, MODE>();
+        for (int k = 0; k < QMAX; ++k) M[k] = IDV;
         int chunk = 0;
+        // rolling slot indices: block L, L-1, L-q, L-q-1  ->  slot (k+1) mod NSB
+        int sL = 1 % NSB, sL1 = 0, sQ = ((1 - q) % NSB + NSB) % NSB, sQ1 = ((-q) % NSB + NSB) % NSB;
+        const unsigned char* rbase = ring + load_off;
         for (int L = 0; L <= Lend; ++L) {
             bar_sync(BAR_VW, NVW * 32);  // iteration L-1 done by every vertical thread
             if (warp == 0 && L + PF <= Lend) issue(L + PF);
-            const int slot = (L + 1) % pl.NSB;
-            mbar_wait(&full[slot], ((L + 1) / pl.NSB) & 1);
+            mbar_wait(&full[sL], ((L + 1) / NSB) & 1);
             const bool emit = L >= Lf;
             const int buf = chunk & 1;
             if (emit) bar_sync(BAR_EMPTY0 + buf, NTH);
             if (active) {
-                const unsigned char* lead = slot_base(L);
-                const int oL = s + L * B - w1;
-                LW<T> out[B];
+                const unsigned char* lead = rbase + (size_t)sL * (B * RP);
+                unsigned char* vb = vt + (size_t)buf * NGC * VTG * ESZ;
+                // store a finished group of GR rows (m0 .. m0+GR-1) of this thread's 2 columns
+                uint32_t grp[GR];
+                auto flush = [&](int m0) {
+                    unsigned char* rowg = vb + (m0 / GR) * VTG * ESZ;
+                    if constexpr (sz == 1) {
+                        if (voff0 >= 0)
+                            *reinterpret_cast<uint2*>(rowg + voff0) =
+                                make_uint2(prmt(grp[0], grp[2], 0x5410), prmt(grp[1], grp[3], 0x5410));
+                        if (voff1 >= 0)
+                            *reinterpret_cast<uint2*>(rowg + voff1) =
+                                make_uint2(prmt(grp[0], grp[2], 0x7632), prmt(grp[1], grp[3], 0x7632));
+                    } else {
+                        if (voff0 >= 0) *reinterpret_cast<uint32_t*>(rowg + voff0) = prmt(grp[0], grp[1], 0x5410);
+                        if (voff1 >= 0) *reinterpret_cast<uint32_t*>(rowg + voff1) = prmt(grp[0], grp[1], 0x7632);
+                    }
+                };
                 if constexpr (VDIRECT) {
                     constexpr int WD = VB;
-                    LW<T> X[B + WD - 1];
-                    const unsigned char* prev = slot_base(L - 1);
+                    uint32_t X[B + WD - 1];
+                    const unsigned char* prev = rbase + (size_t)sL1 * (B * RP);
 #pragma unroll
-                    for (int k = 0; k < WD - 1; ++k) X[k] = ldw(prev + (size_t)(B - (WD - 1) + k) * pl.RP);
+                    for (int k = 0; k < WD - 1; ++k) X[k] = ldw(prev + (B - (WD - 1) + k) * RP);
 #pragma unroll
-                    for (int m = 0; m < B; ++m) X[WD - 1 + m] = ldw(lead + (size_t)m * pl.RP);
+                    for (int m = 0; m < B; ++m) X[WD - 1 + m] = ldw(lead + m * RP);
                     if (emit) {
 #pragma unroll
                         for (int m = 0; m < B; ++m) {
-                            if constexpr (WD == 1) out[m] = X[m];
-                            else if constexpr (WD == 3) out[m] = lop3<MODE>(X[m], X[m + 1], X[m + 2]);
-                            else if constexpr (WD == 5) out[m] = lop3<MODE>(lop3<MODE>(X[m], X[m + 1], X[m + 2]), X[m + 3], X[m + 4]);
-                            else out[m] = lop3<MODE>(lop3<MODE>(X[m], X[m + 1], X[m + 2]), lop3<MODE>(X[m + 3], X[m + 4], X[m + 5]), X[m + 6]);
+                            uint32_t o;
+                            if constexpr (WD == 1) o = X[m];
+                            else if constexpr (WD == 3) o = op3(X[m], X[m + 1], X[m + 2]);
+                            else if constexpr (WD == 5) o = op3(op3(X[m], X[m + 1], X[m + 2]), X[m + 3], X[m + 4]);
+                            else o = op3(op3(X[m], X[m + 1], X[m + 2]), op3(X[m + 3], X[m + 4], X[m + 5]), X[m + 6]);
+                            grp[m % GR] = o;
+                            if (m % GR == GR - 1) flush(m - (GR - 1));
                         }
                     }
                 } else {
-                    LW<T> P[B];
+                    uint32_t P[B];
                     P[0] = ldw(lead);
 #pragma unroll
-                    for (int m = 1; m < B; ++m) P[m] = lop<MODE>(P[m - 1], ldw(lead + (size_t)m * pl.RP));
+                    for (int m = 1; m < B; ++m) P[m] = op2(P[m - 1], ldw(lead + m * RP));
                     if (emit) {
                         // gap = tail r rows of block L-q + whole blocks L-q+1 .. L-1
-                        LW<T> gap = lid<T, MODE>();
-                        const unsigned char* tb = slot_base(L - q);
-                        for (int i = 0; i < r; ++i) gap = lop<MODE>(gap, ldw(tb + (size_t)(B - r + i) * pl.RP));
+                        const unsigned char* tb = rbase + (size_t)sQ * (B * RP);
+                        uint32_t gap = IDV;
+                        for (int i = 0; i < r; ++i) gap = op2(gap, ldw(tb + (B - r + i) * RP));
 #pragma unroll
                         for (int k = 0; k < QMAX - 1; ++k)
-                            if (k < q - 1) gap = lop<MODE>(gap, M[k]);
+                            if (k < q - 1) gap = op2(gap, M[k]);
                         // trailing run rows oL + m: block L-q-1 row B-r+m (m < r), block L-q row m-r
-                        const unsigned char* ta = slot_base(L - q - 1) + (size_t)(B - r) * pl.RP;
-                        const unsigned char* tbb = tb - (size_t)r * pl.RP;
-                        LW<T> acc = gap;
+                        const unsigned char* ta = rbase + (size_t)sQ1 * (B * RP) + (B - r) * RP;
+                        const unsigned char* tbb = tb - r * RP;
+                        uint32_t acc = gap;
 #pragma unroll
                         for (int m = B - 1; m >= 0; --m) {
-                            const unsigned char* a = (m < r ? ta : tbb) + (size_t)m * pl.RP;
-                            acc = lop<MODE>(acc, ldw(a));
-                            out[m] = lop<MODE>(acc, P[m]);
+                            acc = op2(acc, ldw((m < r ? ta : tbb) + m * RP));
+                            grp[m % GR] = op2(acc, P[m]);
+                            if (m % GR == 0) flush(m);
                         }
                     }
 #pragma unroll
                     for (int k = QMAX - 1; k > 0; --k) M[k] = M[k - 1];
                     M[0] = P[B - 1];
                 }
-                if (emit) {
-                    // transpose GR x PX blocks and store into VT[buf] (rows oL.. of this chunk)
-                    unsigned char* vb = vt + (size_t)buf * pl.NGC * pl.VTWE * ESZ;
-#pragma unroll
-                    for (int g = 0; g < B / GR; ++g) {
-                        unsigned char* rowg = vb + (size_t)g * pl.VTWE * ESZ;
-                        const int e0 = PX * t;
-                        if constexpr (sz == 1) {
-                            const LW<uint8_t> r0 = out[4 * g], r1 = out[4 * g + 1], r2 = out[4 * g + 2], r3 = out[4 * g + 3];
-                            *reinterpret_cast<uint2*>(rowg + swz<T>(e0 + 0) * ESZ) =
-                                make_uint2(prmt(r0.a, r2.a, 0x5410), prmt(r1.a, r3.a, 0x5410));
-                            *reinterpret_cast<uint2*>(rowg + swz<T>(e0 + 1) * ESZ) =
-                                make_uint2(prmt(r0.b, r2.b, 0x5410), prmt(r1.b, r3.b, 0x5410));
-                            *reinterpret_cast<uint2*>(rowg + swz<T>(e0 + 2) * ESZ) =
-                                make_uint2(prmt(r0.a, r2.a, 0x7632), prmt(r1.a, r3.a, 0x7632));
-                            *reinterpret_cast<uint2*>(rowg + swz<T>(e0 + 3) * ESZ) =
-                                make_uint2(prmt(r0.b, r2.b, 0x7632), prmt(r1.b, r3.b, 0x7632));
-                        } else {
-                            const LW<uint16_t> r0 = out[2 * g], r1 = out[2 * g + 1];
-                            *reinterpret_cast<uint32_t*>(rowg + swz<T>(e0 + 0) * ESZ) = prmt(r0.a, r1.a, 0x5410);
-                            *reinterpret_cast<uint32_t*>(rowg + swz<T>(e0 + 1) * ESZ) = prmt(r0.a, r1.a, 0x7632);
-                        }
-                    }
-                }
             }
             if (emit) {
                 bar_arrive(BAR_FULL0 + buf, NTH);
                 ++chunk;
             }
+            sL1 = sL;
+            sL = sL + 1 == NSB ? 0 : sL + 1;
+            sQ1 = sQ;
+            sQ = sQ + 1 == NSB ? 0 : sQ + 1;
         }
         // balance the horizontal side's extra releases so every barrier generation completes
         bar_sync(BAR_EMPTY0 + (chunk & 1), NTH);
@@ -408,31 +415,37 @@ morph_stream_kernel(StreamParams p) {
         const int hw = warp - NVW;
         bar_arrive(BAR_EMPTY0 + 0, NTH);
         bar_arrive(BAR_EMPTY0 + 1, NTH);
-        unsigned char* scr = hs + (size_t)hw * (pl.HSE + 64) * ESZ;  // P scratch, then M scratch
-        unsigned char* msc = scr + (size_t)pl.HSE * ESZ;
-        const int off = (x0 - gx) - xs_col;
+        const int sub = lane / LPG;       // row group within the warp pass
+        const int lam = lane % LPG;       // 8-column chunk owned by this lane
+        unsigned char* scr = hs + (size_t)(hw * SUBG + sub) * (VTG + NCHP) * ESZ;  // P scratch, then M
+        unsigned char* msc = scr + (size_t)VTG * ESZ;
+        const int q8 = w1x >> 3, r8 = w1x & 7;
         int chunk = 0;
+        auto ld8 = [&](const unsigned char* a) -> LW<T> {
+            LW<T> v;
+            if constexpr (sz == 1) {
+                const uint2 u = *reinterpret_cast<const uint2*>(a);
+                v.a = u.x;
+                v.b = u.y;
+            } else {
+                v.a = *reinterpret_cast<const uint32_t*>(a);
+            }
+            return v;
+        };
+        auto st8 = [&](unsigned char* a, LW<T> v) {
+            if constexpr (sz == 1) *reinterpret_cast<uint2*>(a) = make_uint2(v.a, v.b);
+            else *reinterpret_cast<uint32_t*>(a) = v.a;
+        };
         for (int L = Lf; L <= Lend; ++L, ++chunk) {
             const int buf = chunk & 1;
             bar_sync(BAR_FULL0 + buf, NTH);
             const int oL = s + L * B - w1;
-            const unsigned char* vb = vt + (size_t)buf * pl.NGC * pl.VTWE * ESZ;
-            for (int g = hw; g < pl.NGC; g += NHW) {
+            const unsigned char* vb = vt + (size_t)buf * NGC * VTG * ESZ;
+            for (int g0 = hw * SUBG; g0 < NGC; g0 += NHW * SUBG) {
+                const int g = g0 + sub;
                 const int o_g = oL + g * GR;
-                if (o_g + GR - 1 < 0 || o_g >= rh) continue;
-                const unsigned char* rowg = vb + (size_t)g * pl.VTWE * ESZ;
-                auto ldv = [&](int xv) -> LW<T> {
-                    LW<T> v;
-                    if constexpr (sz == 1) {
-                        const uint2 u = *reinterpret_cast<const uint2*>(rowg + swz<T>(xv) * ESZ);
-                        v.a = u.x;
-                        v.b = u.y;
-                    } else {
-                        v.a = *reinterpret_cast<const uint32_t*>(rowg + swz<T>(xv) * ESZ);
-                    }
-                    return v;
-                };
-                // emit GR output columns (a..a+GR-1) of rows g*GR.. into the output tile
+                const bool live = g < NGC && o_g + GR - 1 >= 0 && o_g < rh;
+                const unsigned char* rowg = vb + (size_t)(g < NGC ? g : 0) * VTG * ESZ;
                 // emit GR output columns (a..a+GR-1) of rows g*GR.. into the output tile
                 auto emit4 = [&](int a, LW<T> c0, LW<T> c1, LW<T> c2, LW<T> c3) {
                     unsigned char* po = outt + (size_t)(g * GR) * OUTP + (size_t)a * sz;
@@ -448,95 +461,69 @@ morph_stream_kernel(StreamParams p) {
                         *reinterpret_cast<uint32_t*>(po + OUTP) = prmt(c0.a, c1.a, 0x7632);
                     }
                 };
+                auto emit8 = [&](const LW<T> (&o)[8]) {
+#pragma unroll
+                    for (int j = 0; j < 8; j += GR) {
+                        if constexpr (GR == 4) emit4(8 * lam + j, o[j], o[j + 1], o[j + 2], o[j + 3]);
+                        else emit4(8 * lam + j, o[j], o[j + 1], o[j], o[j]);
+                    }
+                };
                 if constexpr (HB <= 7) {
-                    // direct window: each lane owns TW/32 consecutive output columns
+                    // direct window: lane owns 8 output columns; position 8*lam + i, i < 8 + WD - 1
                     constexpr int WD = HB;
-                    constexpr int NO = TW / 32;
-                    LW<T> X[NO + WD - 1];
-                    const int a0 = lane * NO;
+                    LW<T> X[8 + WD - 1];
+                    const unsigned char* b0 = rowg + lam * ESZ;
 #pragma unroll
-                    for (int i = 0; i < NO + WD - 1; ++i) X[i] = ldv(off + a0 + i);
-                    LW<T> o[NO];
+                    for (int i = 0; i < 8 + WD - 1; ++i)
+                        X[i] = ld8(b0 + ((i & 7) * NCHP + (i >> 3)) * ESZ);
+                    LW<T> o[8];
 #pragma unroll
-                    for (int j = 0; j < NO; ++j) {
+                    for (int j = 0; j < 8; ++j) {
                         if constexpr (WD == 1) o[j] = X[j];
                         else if constexpr (WD == 3) o[j] = lop3<MODE>(X[j], X[j + 1], X[j + 2]);
                         else if constexpr (WD == 5) o[j] = lop3<MODE>(lop3<MODE>(X[j], X[j + 1], X[j + 2]), X[j + 3], X[j + 4]);
                         else o[j] = lop3<MODE>(lop3<MODE>(X[j], X[j + 1], X[j + 2]), lop3<MODE>(X[j + 3], X[j + 4], X[j + 5]), X[j + 6]);
                     }
-#pragma unroll
-                    for (int j = 0; j < NO; j += GR) {
-                        if constexpr (GR == 4) emit4(a0 + j, o[j], o[j + 1], o[j + 2], o[j + 3]);
-                        else emit4(a0 + j, o[j], o[j + 1], o[j], o[j]);
-                    }
+                    if (live) emit8(o);
                 } else {
-                    // lane-chunk van Herk: chunk k = inputs [kC, kC+C); prefix -> scratch, suffix kept
-                    constexpr int C = HC;
-                    const int nch = (TW + w1x + C - 1) / C;
-                    LW<T> S[C];
-                    for (int k = lane; k < nch; k += 32) {
-                        LW<T> x[C];
+                    // lane-chunk van Herk over 8-column chunks: prefix -> scratch, suffix in registers
+                    const int nch = (TW + w1x + 7) >> 3;
+                    LW<T> S[8];
+                    for (int k = lam; k < nch; k += LPG) {
+                        LW<T> x[8];
+                        const unsigned char* b0 = rowg + k * ESZ;
 #pragma unroll
-                        for (int j = 0; j < C; ++j) x[j] = ldv(off + k * C + j);
+                        for (int j = 0; j < 8; ++j) x[j] = ld8(b0 + j * NCHP * ESZ);
                         LW<T> pre = x[0];
+                        unsigned char* pb = scr + k * ESZ;
 #pragma unroll
-                        for (int j = 0; j < C; ++j) {
+                        for (int j = 0; j < 8; ++j) {
                             if (j) pre = lop<MODE>(pre, x[j]);
-                            if constexpr (sz == 1)
-                                *reinterpret_cast<uint2*>(scr + swz<T>(k * C + j) * ESZ) = make_uint2(pre.a, pre.b);
-                            else
-                                *reinterpret_cast<uint32_t*>(scr + swz<T>(k * C + j) * ESZ) = pre.a;
+                            st8(pb + j * NCHP * ESZ, pre);
                         }
-                        if constexpr (sz == 1)
-                            *reinterpret_cast<uint2*>(msc + k * ESZ) = make_uint2(pre.a, pre.b);
-                        else
-                            *reinterpret_cast<uint32_t*>(msc + k * ESZ) = pre.a;
-                        if (k == lane) {
-                            S[C - 1] = x[C - 1];
+                        st8(msc + k * ESZ, pre);
+                        if (k == lam) {
+                            S[7] = x[7];
 #pragma unroll
-                            for (int j = C - 2; j >= 0; --j) S[j] = lop<MODE>(S[j + 1], x[j]);
+                            for (int j = 6; j >= 0; --j) S[j] = lop<MODE>(S[j + 1], x[j]);
                         }
                     }
                     __syncwarp();
-                    const int k = lane;
-                    if (k * C < TW) {
-                        const int qc = w1x / C, rc = w1x - qc * C;
-                        auto ldm = [&](int kk) -> LW<T> {
-                            LW<T> v;
-                            if constexpr (sz == 1) {
-                                const uint2 u = *reinterpret_cast<const uint2*>(msc + kk * ESZ);
-                                v.a = u.x;
-                                v.b = u.y;
-                            } else {
-                                v.a = *reinterpret_cast<const uint32_t*>(msc + kk * ESZ);
-                            }
-                            return v;
-                        };
-                        auto ldp = [&](int e) -> LW<T> {
-                            LW<T> v;
-                            if constexpr (sz == 1) {
-                                const uint2 u = *reinterpret_cast<const uint2*>(scr + swz<T>(e) * ESZ);
-                                v.a = u.x;
-                                v.b = u.y;
-                            } else {
-                                v.a = *reinterpret_cast<const uint32_t*>(scr + swz<T>(e) * ESZ);
-                            }
-                            return v;
-                        };
+                    {
+                        const int k = lam;
                         LW<T> Fa = lid<T, MODE>();
-                        for (int i = 1; i < qc; ++i) Fa = lop<MODE>(Fa, ldm(k + i));
-                        const LW<T> Fb = lop<MODE>(Fa, ldm(k + qc));
-                        LW<T> o[C];
+                        for (int i = 1; i < q8; ++i) Fa = lop<MODE>(Fa, ld8(msc + (k + i) * ESZ));
+                        const LW<T> Fb = lop<MODE>(Fa, ld8(msc + (k + q8) * ESZ));
+                        // P at position 8k + j + w1x: chunk k+q8 (+1), index (j + r8) & 7
+                        const unsigned char* pa = scr + (r8 * NCHP + k + q8) * ESZ;
+                        const unsigned char* pbb = scr + ((r8 - 8) * NCHP + k + q8 + 1) * ESZ;
+                        LW<T> o[8];
 #pragma unroll
-                        for (int j = 0; j < C; ++j) {
-                            const int a = k * C + j;
-                            o[j] = lop3<MODE>(S[j], j < C - rc ? Fa : Fb, ldp(a + w1x));
+                        for (int j = 0; j < 8; ++j) {
+                            const bool lo = j < 8 - r8;
+                            o[j] = lop3<MODE>(S[j], lo ? Fa : Fb, ld8((lo ? pa : pbb) + j * NCHP * ESZ));
                         }
-#pragma unroll
-                        for (int j = 0; j < C; j += GR) {
-                            if constexpr (GR == 4) emit4(k * C + j, o[j], o[j + 1], o[j + 2], o[j + 3]);
-                            else emit4(k * C + j, o[j], o[j + 1], o[j], o[j]);
-                        }
+                        if (live) emit8(o);
                     }
                     __syncwarp();
                 }
@@ -545,7 +532,7 @@ morph_stream_kernel(StreamParams p) {
             bar_sync(BAR_HW, NHW * 32);
             // store the valid rows of the chunk
             {
-                const int htid = tid - NVW * 32;
+                const int htid = tid - NVW * 32;  // horizontal thread index
                 const int cols = min(TW, p.W - x0);
                 const int row_bytes = cols * sz;
                 const bool vec = (((uintptr_t)dst | p.dp) & 15) == 0 && cols == TW;
@@ -589,18 +576,18 @@ cudaError_t launch_stream_variant(const MorphJob& j, int rh, int B, int q) {
     p.simg = j.simg;
     p.dimg = j.dimg;
     p.rh = rh;
-    const Plan pl = make_plan<T>(B, q, j.gx, HB > 7);
+    const Plan pl = make_plan<T, HB>(B, q);
     auto kern = morph_stream_kernel<T, MODE, VB, HB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
     if (e != cudaSuccess) return e;
     dim3 grid(cdiv(j.W, G::TW), cdiv(j.H, rh), j.batch);
-    kern<<<grid, NTH, pl.total, j.stream>>>(p);
+    kern<<<grid, HG<T, HB>::NTH, pl.total, j.stream>>>(p);
     count_launch();
     return cudaGetLastError();
 }
 
 #define RM_STREAM_V(X) X(1) X(3) X(5) X(7) X(8) X(16) X(24)
-#define RM_STREAM_H(X) X(1) X(3) X(5) X(7) X(8)
+#define RM_STREAM_H(X) X(1) X(3) X(5) X(7) X(8) X(9)
 
 template <typename T, int MODE, int VB>
 cudaError_t stream_dispatch_h(const MorphJob& j, int hb, int rh, int B, int q) {
@@ -622,6 +609,24 @@ cudaError_t stream_dispatch(const MorphJob& j, int vb, int hb, int rh, int B, in
 #undef RM_CASE
     }
     return cudaErrorInvalidValue;
+}
+
+// Host-side planning helpers shared with morph_stream.cu
+inline int stream_gxmax(int elem, int hb) {
+    return elem == 1 ? (hb <= 7 ? (hb - 1) / 2 : hb == 8 ? HG<uint8_t, 8>::GXMAX : HG<uint8_t, 9>::GXMAX)
+                     : (hb <= 7 ? (hb - 1) / 2 : hb == 8 ? HG<uint16_t, 8>::GXMAX : HG<uint16_t, 9>::GXMAX);
+}
+
+template <typename T>
+inline int stream_smem(int hb, int B, int q) {
+    switch (hb) {
+    case 1: return make_plan<T, 1>(B, q).total;
+    case 3: return make_plan<T, 3>(B, q).total;
+    case 5: return make_plan<T, 5>(B, q).total;
+    case 7: return make_plan<T, 7>(B, q).total;
+    case 8: return make_plan<T, 8>(B, q).total;
+    default: return make_plan<T, 9>(B, q).total;
+    }
 }
 
 }  // namespace stream
