@@ -302,6 +302,8 @@ morph_stream_kernel(StreamParams p) {
         if (warp == 0) {
             for (int k = -1; k < PF && k <= Lend; ++k) issue(k);
         }
+        // block -1 is never a leading block: wait for it once before its rows are read as trailing
+        mbar_wait(&full[0], 0);
 
         auto ldw = [&](const unsigned char* a) -> uint32_t {
             if constexpr (sz == 1) {
