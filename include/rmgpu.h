@@ -172,6 +172,9 @@ unsigned long long rmgpu_launch_count(void);
 /* Name of the kernel variant the planner picks for a morph call (for tests / profiling);
  * returns a static string. elem_bytes 1 or 2. */
 const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int wy, int op);
+/* Debug: clock64 timeline of one CTA of the streaming kernel into a device buffer of >= 1024
+ * int64 (NULL disables). Not part of the reference API. */
+void rmgpu_debug_trace(void* device_buf, int cta);
 
 #ifdef __cplusplus
 }

@@ -45,12 +45,14 @@ SIGNATURES = {
     "rmgpu_status_string": [_I],
     "rmgpu_launch_count": [],
     "rmgpu_plan_name": [_I, _I, _I, _I, _I, _I],
+    "rmgpu_debug_trace": [_P, _I],
 }
 _RESTYPES = {
     "rmgpu_last_error": C.c_char_p,
     "rmgpu_status_string": C.c_char_p,
     "rmgpu_launch_count": C.c_ulonglong,
     "rmgpu_plan_name": C.c_char_p,
+    "rmgpu_debug_trace": None,
 }
 
 _lock = threading.Lock()

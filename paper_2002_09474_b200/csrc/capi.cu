@@ -327,6 +327,10 @@ const char* rmgpu_status_string(int status) {
 
 unsigned long long rmgpu_launch_count(void) { return rmgpu::g_launch_count.load(); }
 
+// Debug: record a clock64 timeline of one CTA of the streaming kernel into a device buffer of
+// >= 1024 int64 (nullptr disables). Not part of the reference API.
+void rmgpu_debug_trace(void* device_buf, int cta) { rmgpu::stream::set_trace((long long*)device_buf, cta); }
+
 int rmgpu_resolve(int algo, int window, int axis, int threshold_h, int threshold_v) {
     if (algo != RMGPU_ALGO_AUTO) return algo;  // dispatch.cpp:14-20
     const int t = axis == RMGPU_AXIS_HORIZONTAL ? threshold_h : threshold_v;

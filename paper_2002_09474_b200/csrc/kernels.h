@@ -45,6 +45,7 @@ const char* fast_plan_name(const MorphJob& j);
 namespace stream {
 bool launch(const MorphJob& j, cudaError_t* err);
 const char* plan_name(const MorphJob& j);
+void set_trace(long long* device_buf, int cta);  // debug timeline (tools/trace_stream.py)
 }  // namespace stream
 
 // ---- transposes (transpose.cu) ---------------------------------------------------------------

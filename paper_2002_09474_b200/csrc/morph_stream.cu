@@ -22,20 +22,24 @@
 //     from HBM once and written once (halo rows/columns are re-read from L2 by neighbours).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "morph_stream.cuh"
 
 namespace rmgpu {
 namespace stream {
-cudaError_t dispatch_u8_min(const MorphJob&, int, int, int, int, int);
-cudaError_t dispatch_u8_max(const MorphJob&, int, int, int, int, int);
-cudaError_t dispatch_u16_min(const MorphJob&, int, int, int, int, int);
-cudaError_t dispatch_u16_max(const MorphJob&, int, int, int, int, int);
+long long* g_trace = nullptr;
+int g_trace_cta = 0;
+cudaError_t dispatch_u8_min(const MorphJob&, int, int, int, int, int, int);
+cudaError_t dispatch_u8_max(const MorphJob&, int, int, int, int, int, int);
+cudaError_t dispatch_u16_min(const MorphJob&, int, int, int, int, int, int);
+cudaError_t dispatch_u16_max(const MorphJob&, int, int, int, int, int, int);
 
 namespace {
 
 struct Choice {
-    int vb, hb, B, q, rh, smem;
+    int vb, hb, B, q, rh, smem, pf;
 };
 
 bool choose(const MorphJob& j, Choice* c) {
@@ -67,8 +71,28 @@ bool choose(const MorphJob& j, Choice* c) {
     }
     c->hb = j.gx <= 3 ? 2 * j.gx + 1 : (j.gx <= stream_gxmax(j.elem, 8) ? 8 : 9);
     if (j.gx > stream_gxmax(j.elem, c->hb)) return false;
-    const int total = j.elem == 1 ? stream_smem<uint8_t>(c->hb, c->B, c->q) : stream_smem<uint16_t>(c->hb, c->B, c->q);
+    // TMA prefetch depth: keep ~56 KB of input in flight per SM (Little's law at ~1 us DRAM
+    // latency under load and 6.5 TB/s over 148 SMs), within the shared-memory budget.
+    const int blk = c->B * (j.elem == 1 ? stream_ring_row<uint8_t>(c->hb) : stream_ring_row<uint16_t>(c->hb));
+    auto smem_of = [&](int pf) {
+        return j.elem == 1 ? stream_smem<uint8_t>(c->hb, c->B, c->q, pf) : stream_smem<uint16_t>(c->hb, c->B, c->q, pf);
+    };
+    int pf = 2, total = smem_of(pf);
     if (total > 220 * 1024) return false;
+    if (const char* e = getenv("RMGPU_STREAM_PF")) {
+        pf = std::max(1, atoi(e));
+        total = smem_of(pf);
+    } else {
+        for (int cand = 2; cand <= 12; ++cand) {
+            const int t = smem_of(cand);
+            if (t > 220 * 1024) break;
+            const int occ = std::max(1, std::min(8, (227 * 1024) / (t + 1024)));
+            pf = cand;
+            total = t;
+            if ((long)cand * blk * occ >= 56 * 1024) break;
+        }
+    }
+    c->pf = pf;
     c->smem = total;
     // rows per CTA: enough CTAs for ~2 waves of the resident capacity, long runs for big windows
     const int occ = std::max(1, std::min(8, (227 * 1024) / (total + 1024)));
@@ -78,6 +102,10 @@ bool choose(const MorphJob& j, Choice* c) {
     int rh = (int)((j.H + splits - 1) / splits);
     rh = std::max(rh, std::min(j.H, std::max(64, 2 * w1)));
     rh = (rh + 3) / 4 * 4;
+    if (const char* e = getenv("RMGPU_STREAM_RH")) {  // tuning hook
+        const int v = atoi(e);
+        if (v > 0) rh = (v + 3) / 4 * 4;
+    }
     c->rh = rh;
     return true;
 }
@@ -88,10 +116,52 @@ bool launch(const MorphJob& j, cudaError_t* err) {
     Choice c;
     if (!choose(j, &c)) return false;
     if (j.elem == 1)
-        *err = j.mode == MODE_MIN ? dispatch_u8_min(j, c.vb, c.hb, c.rh, c.B, c.q) : dispatch_u8_max(j, c.vb, c.hb, c.rh, c.B, c.q);
+        *err = j.mode == MODE_MIN ? dispatch_u8_min(j, c.vb, c.hb, c.rh, c.B, c.q, c.pf) : dispatch_u8_max(j, c.vb, c.hb, c.rh, c.B, c.q, c.pf);
     else
-        *err = j.mode == MODE_MIN ? dispatch_u16_min(j, c.vb, c.hb, c.rh, c.B, c.q) : dispatch_u16_max(j, c.vb, c.hb, c.rh, c.B, c.q);
+        *err = j.mode == MODE_MIN ? dispatch_u16_min(j, c.vb, c.hb, c.rh, c.B, c.q, c.pf) : dispatch_u16_max(j, c.vb, c.hb, c.rh, c.B, c.q, c.pf);
     return true;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+bool encode_input_map(const MorphJob& j, int box_words, int box_rows, CUtensorMap* map) {
+    memset(map, 0, sizeof(*map));
+    if (getenv("RMGPU_NO_TMA")) return false;
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const size_t row_bytes = (size_t)j.W * j.elem;
+    const long rows = (long)j.above + j.H + j.below;
+    if (j.sp % 16 || (j.batch > 1 && j.simg % 16) || rows < 1) return false;
+    const uint8_t* base = static_cast<const uint8_t*>(j.src) - (ptrdiff_t)j.above * (ptrdiff_t)j.sp;
+    if (reinterpret_cast<uintptr_t>(base) & 15) return false;
+    cuuint64_t dims[3] = {(row_bytes + 3) / 4, (cuuint64_t)rows, (cuuint64_t)std::max(1, j.batch)};
+    cuuint64_t strides[2] = {j.sp, j.batch > 1 ? j.simg : j.sp * (cuuint64_t)rows};
+    cuuint32_t box[3] = {(cuuint32_t)box_words, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint8_t*>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+void set_trace(long long* buf, int cta) {
+    g_trace = buf;
+    g_trace_cta = cta;
 }
 
 const char* plan_name(const MorphJob& j) {
@@ -101,8 +171,8 @@ const char* plan_name(const MorphJob& j) {
     k.sp = (size_t)((j.W * j.elem + 15) / 16 * 16);
     Choice c;
     if (!choose(k, &c)) return nullptr;
-    snprintf(buf, sizeof(buf), "stream_%s_v%s%d_h%s%d_rh%d_smem%dK", j.elem == 1 ? "u8" : "u16", c.vb <= 7 ? "d" : "b",
-             c.vb, c.hb <= 7 ? "d" : "b", c.hb, c.rh, c.smem / 1024);
+    snprintf(buf, sizeof(buf), "stream_%s_v%s%d_h%s%d_rh%d_pf%d_smem%dK", j.elem == 1 ? "u8" : "u16",
+             c.vb <= 7 ? "d" : "b", c.vb, c.hb <= 7 ? "d" : "b", c.hb, c.rh, c.pf, c.smem / 1024);
     return buf;
 }
 

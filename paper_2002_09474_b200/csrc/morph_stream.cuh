@@ -2,16 +2,20 @@
 // erosion / dilation (u8, u16). Design notes in morph_stream.cu.
 #pragma once
 
+#include <algorithm>
+
+#include <cuda.h>  // CUtensorMap (type only; encoded through the runtime's driver entry point)
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace rmgpu {
 namespace stream {
 
-constexpr int NHW = 4;                 // horizontal warps (vertical warp count depends on the class)
-constexpr int PF = 2;                  // input blocks prefetched ahead of the leading block
+// horizontal warps: one per 4-row group of a chunk of B rows (2..8)
+__host__ __device__ constexpr int nhw_of(int B) { return B / 4 < 2 ? 2 : (B / 4 > 8 ? 8 : B / 4); }
 constexpr int QMAX = 6;                // whole blocks between suffix run and prefix block (registers)
-constexpr int VCH = 16;                // rows per iteration for the direct vertical variants
+constexpr int VCH = 32;                // rows per iteration for the direct vertical variants
 constexpr int HC = 8;                  // horizontal lane chunk (block variant)
 
 // named barrier ids (0 is __syncthreads)
@@ -102,6 +106,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(saddr(bar))
                  : "memory");
 }
+// One TMA tensor copy of a box {RP/4 words, B rows} (3-D map: words, rows, images).
+__device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            saddr(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(saddr(bar))
+        : "memory");
+}
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
@@ -120,7 +132,18 @@ struct StreamParams {
     uint32_t bval;
     size_t simg, dimg;
     int rh;               // output rows per CTA
+    int pf;               // input blocks prefetched ahead of the leading block (TMA bytes in flight)
+    long long* trace;     // debug timeline (nullptr normally): CTA (trace_cta) records clock64 stamps
+    int trace_cta;
+    int use_tma;          // interior blocks through one 2-D tensor copy (map rows start at row_lo)
+    int batch;            // images
 };
+
+#define RM_TRACE(slot)                                                                                   \
+    do {                                                                                                 \
+        if (p.trace && blockIdx.x == (unsigned)p.trace_cta && (threadIdx.x & 31) == 0) \
+            p.trace[(slot)] = clock64();                                                                 \
+    } while (0)
 
 // Compile-time geometry of one horizontal class HB: 1/3/5/7 = direct window (gx = (HB-1)/2),
 // 8 / 9 = lane-chunk block algorithm for gx up to GXMAX (small / large halo).
@@ -135,7 +158,6 @@ struct HG {
     static constexpr int VTG = 8 * NCHP;                                     // entries per row group
     static constexpr int LPG = TW / 8;                                       // lanes per row group
     static constexpr int NVW = (RP / (2 * sz) + 31) / 32;                    // vertical warps (2 px/thread)
-    static constexpr int NTH = 32 * (NVW + NHW);                             // threads per CTA
 };
 
 // Shared-memory plan, identical on host and device (B and q runtime -> NSB; rest compile-time).
@@ -144,7 +166,7 @@ struct Plan {
 };
 
 template <typename T, int HB>
-__host__ __device__ inline Plan make_plan(int B, int q) {
+__host__ __device__ inline Plan make_plan(int B, int q, int PF) {
     using H = HG<T, HB>;
     using G = SG<T>;
     Plan p;
@@ -155,7 +177,7 @@ __host__ __device__ inline Plan make_plan(int B, int q) {
     p.off_vt = o;
     o += 2 * (B / G::GR) * H::VTG * G::ESZ;
     p.off_hs = o;
-    if (HB > 7) o += NHW * (32 / H::LPG) * (H::VTG + H::NCHP) * G::ESZ;
+    if (HB > 7) o += nhw_of(B) * (32 / H::LPG) * (H::VTG + H::NCHP) * G::ESZ;
     p.off_out = o;
     o += B * (G::TW * (int)sizeof(T) + 16);
     p.total = o;
@@ -192,49 +214,84 @@ __device__ __forceinline__ uint32_t nib_at(uint32_t nib, int k) { return (nib >>
 // ---- the kernel ------------------------------------------------------------------------------
 // VB: vertical variant: 1/3/5/7 = direct window (VCH rows per iteration), 8/16/24 = block size B.
 // HB: horizontal class (HG).
+template <typename T, int VB, int HB>
+struct KG {  // per-kernel thread layout
+    static constexpr int B = VB <= 7 ? VCH : VB;
+    static constexpr int NHW = nhw_of(B);
+    static constexpr int NVW = HG<T, HB>::NVW;
+    static constexpr int NTH = 32 * (NVW + NHW);
+};
+
+// Work item = (strip, row range, image); items are processed persistently by the CTAs of a 1-D
+// grid (CTA c takes items c, c + G, ...), and the TMA block stream runs on across items so the
+// next item's first rows arrive while the current one finishes.
+struct Item {
+    int x0, y0, rh, b;
+    int xs_b, xs_col, copy_len, cb0, nwv, off, y_first, Lend, Lf;
+};
+
+template <typename T>
+__device__ __forceinline__ Item make_item(const StreamParams& p, int idx, int nstrips, int nrowb, int B, int w1,
+                                          int s) {
+    constexpr int TW = SG<T>::TW, sz = sizeof(T);
+    Item it;
+    const int per_img = nstrips * nrowb;
+    it.b = idx / per_img;
+    const int rem = idx - it.b * per_img;
+    const int ry = rem / nstrips;
+    it.x0 = (rem - ry * nstrips) * TW;
+    it.y0 = ry * p.rh;
+    it.rh = min(p.rh, p.H - it.y0);
+    const int xb = (it.x0 - p.gx) * sz;
+    it.xs_b = xb >= 0 ? (xb / 16) * 16 : -(((-xb) + 15) / 16) * 16;
+    it.xs_col = it.xs_b / sz;
+    const int xe_b = ((it.x0 + TW + p.gx) * sz + 15) / 16 * 16;
+    const int w_b16 = (p.W * sz + 15) / 16 * 16;
+    it.cb0 = max(it.xs_b, 0);
+    it.copy_len = min(xe_b, w_b16) - it.cb0;
+    it.nwv = (xe_b - it.xs_b) / (2 * sz);
+    it.off = (it.x0 - p.gx) - it.xs_col;
+    it.y_first = it.y0 - p.gy;
+    it.Lend = (it.rh - 1 + w1 - s) / B;
+    int Lf = 0;
+    while (s + Lf * B - w1 + B - 1 < 0) ++Lf;
+    it.Lf = Lf;
+    return it;
+}
+
+template <int MODE>
+__device__ __forceinline__ uint32_t tree_min(uint32_t a, uint32_t b, uint32_t c) {
+    return red3_u16x2<MODE>(a, b, c);
+}
+
 template <typename T, int MODE, int VB, int HB>
-__global__ void __launch_bounds__(HG<T, HB>::NTH)
-morph_stream_kernel(StreamParams p) {
+__global__ void __launch_bounds__(KG<T, VB, HB>::NTH)
+morph_stream_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tmap) {
     using G = SG<T>;
     using H = HG<T, HB>;
-    constexpr int PX = G::PX, GR = G::GR, TW = G::TW, ESZ = G::ESZ;
+    constexpr int GR = G::GR, TW = G::TW, ESZ = G::ESZ;
     constexpr int sz = sizeof(T);
     constexpr bool VDIRECT = VB <= 7;
     constexpr int B = VDIRECT ? VCH : VB;
     constexpr int NGC = B / GR;          // row groups per chunk
     constexpr int OUTP = TW * sz + 16;
     constexpr int RP = H::RP, NCHP = H::NCHP, VTG = H::VTG, LPG = H::LPG;
-    constexpr int NVW = H::NVW, NTH = H::NTH;
+    constexpr int NVW = KG<T, VB, HB>::NVW, NTH = KG<T, VB, HB>::NTH, NHW = KG<T, VB, HB>::NHW;
     constexpr int SUBG = 32 / LPG;       // row groups per warp pass
     extern __shared__ __align__(128) unsigned char smem[];
 
-    const int gx = p.gx, gy = p.gy;
-    const int w1 = 2 * gy, w1x = 2 * gx;
+    const int gy = p.gy;
+    const int w1 = 2 * gy, w1x = 2 * p.gx;
     const int q = VDIRECT ? 0 : w1 / B;
     const int r = VDIRECT ? w1 : w1 - q * B;
     const int s = r & 3;
-    const Plan pl = make_plan<T, HB>(B, q);
+    const int PF = p.pf;
+    const Plan pl = make_plan<T, HB>(B, q, PF);
     const int NSB = pl.NSB;
-
-    const uint8_t* src = p.src + blockIdx.z * p.simg;
-    uint8_t* dst = p.dst + blockIdx.z * p.dimg;
-    const int x0 = blockIdx.x * TW;
-    const int y0 = blockIdx.y * p.rh;
-    const int rh = min(p.rh, p.H - y0);
-    // strip bytes [xs_b, xe_b) of every input row, 16-byte aligned
-    const int xb = (x0 - gx) * sz;
-    const int xs_b = xb >= 0 ? (xb / 16) * 16 : -(((-xb) + 15) / 16) * 16;
-    const int xs_col = xs_b / sz;
-    const int xe_b = ((x0 + TW + gx) * sz + 15) / 16 * 16;
-    const int w_b16 = (p.W * sz + 15) / 16 * 16;
-    const int cb0 = max(xs_b, 0);
-    const int copy_len = min(xe_b, w_b16) - cb0;  // bytes copied per row (multiple of 16)
-    const int nwv = (xe_b - xs_b) / (2 * sz);     // 2-pixel column words
-    const int off = (x0 - gx) - xs_col;           // horizontal input position 0 = strip column off
-    const int y_first = y0 - gy;                  // image row of input index 0
-    const int Lend = (rh - 1 + w1 - s) / B;
-    int Lf = 0;
-    while (s + Lf * B - w1 + B - 1 < 0) ++Lf;
+    const int nstrips = (p.W + TW - 1) / TW;
+    const int nrowb = (p.H + p.rh - 1) / p.rh;
+    const int nitems = nstrips * nrowb * p.batch;
+    const int G0 = (int)gridDim.x;
 
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     unsigned char* ring = smem + pl.off_ring;
@@ -252,162 +309,217 @@ morph_stream_kernel(StreamParams p) {
     __syncthreads();
 
     const int warp = tid >> 5, lane = tid & 31;
+    auto item_at = [&](int n) { return (int)blockIdx.x + n * G0; };  // n-th item of this CTA
 
     if (warp < NVW) {
         // ================= vertical role: producer (warp 0) + streaming column sweeps =========
-        // thread t owns image columns xs_col + 2t, +1 as one u16x2 word (u8 unpacked on load)
-        const int t = tid;
-        const bool active = t < nwv;
-        int load_off = 0;
-        uint32_t nib = 0;
-        bool fix = false;
-        col_fix<T>(xs_col + 2 * (active ? t : 0), p.W, p.cmode, xs_col, load_off, nib, fix);
-        // u8: unpack + border fix in one PRMT over (raw16, Z), Z = {bval, 0, 0, 0}
-        const uint32_t selU = sz == 1 ? ((nib & 0xF) | (5u << 4) | (((nib >> 4) & 0xF) << 8) | (5u << 12)) : nib;
-        const uint32_t Z = bv;  // u16: bytes {lo, hi, 0, 0} -> nibbles 4, 5
-
-        // VT destinations of this thread's 2 columns (position = column - off), -1 = unused
-        int voff0, voff1;
-        {
-            const int pos0 = 2 * t - off, pos1 = pos0 + 1;
-            voff0 = (active && pos0 >= 0 && pos0 < 8 * H::NCH) ? ((pos0 & 7) * NCHP + (pos0 >> 3)) * ESZ : -1;
-            voff1 = (active && pos1 >= 0 && pos1 < 8 * H::NCH) ? ((pos1 & 7) * NCHP + (pos1 >> 3)) * ESZ : -1;
-        }
-
-        // issue block k (rows [s + kB, s + kB + B) of the input index space) into its slot
-        auto issue = [&](int k) {
-            const int slot = (k + 1) % NSB;
+        // ---- producer cursor (warp 0): block pk of this CTA's item pn ------------------------
+        int pn = 0, pk = -1;
+        Item pit;
+        bool pvalid = item_at(0) < nitems;
+        if (pvalid) pit = make_item<T>(p, item_at(0), nstrips, nrowb, B, w1, s);
+        int pslot = 0;  // ring slot of the next block to issue
+        auto issue_next = [&]() {
+            if (!pvalid) return;
+            const int slot = pslot;
             unsigned char* base = ring + (size_t)slot * B * RP;
-            const int y = y_first + s + k * B + lane;
-            const bool inrow = lane < B;
-            const bool outside = p.cmode && (y < p.row_lo || y >= p.row_hi);
-            const unsigned cp = __ballot_sync(0xffffffffu, inrow && !outside);
-            unsigned fillm = __ballot_sync(0xffffffffu, inrow && outside);
-            while (fillm) {  // constant rows outside the image: the warp writes the border value
-                const int m = __ffs(fillm) - 1;
-                fillm &= fillm - 1;
-                const uint32_t bw = sz == 1 ? bv * 0x01010101u : bv * 0x00010001u;
-                uint4* row = reinterpret_cast<uint4*>(base + (size_t)m * RP);
-                for (int c = lane; c < RP / 16; c += 32) row[c] = make_uint4(bw, bw, bw, bw);
+            const int yb = pit.y_first + s + pk * B;
+            if (p.use_tma && yb >= p.row_lo && yb + B <= p.row_hi) {
+                if (lane == 0) {
+                    mbar_arrive_tx(&full[slot], (uint32_t)(B * RP));
+                    tma_box(base, &tmap, pit.xs_b / 4, yb - p.row_lo, pit.b, &full[slot]);
+                }
+            } else {
+                const uint8_t* src = p.src + (size_t)pit.b * p.simg;
+                const int y = yb + lane;
+                const bool inrow = lane < B;
+                const bool outside = p.cmode && (y < p.row_lo || y >= p.row_hi);
+                const unsigned cp = __ballot_sync(0xffffffffu, inrow && !outside);
+                unsigned fillm = __ballot_sync(0xffffffffu, inrow && outside);
+                while (fillm) {  // constant rows outside the image: the warp writes the border value
+                    const int m = __ffs(fillm) - 1;
+                    fillm &= fillm - 1;
+                    const uint32_t bw = sz == 1 ? bv * 0x01010101u : bv * 0x00010001u;
+                    uint4* row = reinterpret_cast<uint4*>(base + (size_t)m * RP);
+                    for (int c = lane; c < RP / 16; c += 32) row[c] = make_uint4(bw, bw, bw, bw);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive_tx(&full[slot], (uint32_t)(__popc(cp) * pit.copy_len));
+                __syncwarp();
+                if (inrow && !outside) {
+                    const int yc = min(max(y, p.row_lo), p.row_hi - 1);
+                    bulk_g2s(base + (size_t)lane * RP + (pit.cb0 - pit.xs_b),
+                             src + (ptrdiff_t)yc * (ptrdiff_t)p.sp + pit.cb0, (uint32_t)pit.copy_len, &full[slot]);
+                }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_tx(&full[slot], (uint32_t)(__popc(cp) * copy_len));
-            __syncwarp();
-            if (inrow && !outside) {
-                const int yc = min(max(y, p.row_lo), p.row_hi - 1);
-                bulk_g2s(base + (size_t)lane * RP + (cb0 - xs_b), src + (ptrdiff_t)yc * (ptrdiff_t)p.sp + cb0,
-                         (uint32_t)copy_len, &full[slot]);
+            pslot = pslot + 1 == NSB ? 0 : pslot + 1;
+            if (++pk > pit.Lend) {
+                ++pn;
+                pk = -1;
+                pvalid = item_at(pn) < nitems;
+                if (pvalid) pit = make_item<T>(p, item_at(pn), nstrips, nrowb, B, w1, s);
             }
         };
         if (warp == 0) {
-            for (int k = -1; k < PF && k <= Lend; ++k) issue(k);
+            if (lane == 0 && p.use_tma) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
+            for (int k = 0; k <= PF; ++k) issue_next();  // blocks seq 0 .. PF
         }
-        // block -1 is never a leading block: wait for it once before its rows are read as trailing
-        mbar_wait(&full[0], 0);
 
-        auto ldw = [&](const unsigned char* a) -> uint32_t {
-            if constexpr (sz == 1) {
-                const uint32_t raw = *reinterpret_cast<const uint16_t*>(a);
-                return prmt(raw, Z, selU);
-            } else {
-                const uint32_t raw = *reinterpret_cast<const uint32_t*>(a);
-                return fix ? prmt(raw, Z, selU) : raw;
-            }
-        };
         auto op2 = [](uint32_t x, uint32_t y) { return red2_u16x2<MODE>(x, y); };
         auto op3 = [](uint32_t x, uint32_t y, uint32_t z) { return red3_u16x2<MODE>(x, y, z); };
         constexpr uint32_t IDV = MODE == MODE_MIN ? 0xFFFFFFFFu : 0u;
 
-        uint32_t M[QMAX];
-#pragma unroll
-        for (int k = 0; k < QMAX; ++k) M[k] = IDV;
-        int chunk = 0;
-        // rolling slot indices: block L, L-1, L-q, L-q-1  ->  slot (k+1) mod NSB
-        int sL = 1 % NSB, sL1 = 0, sQ = ((1 - q) % NSB + NSB) % NSB, sQ1 = ((-q) % NSB + NSB) % NSB;
-        const unsigned char* rbase = ring + load_off;
-        for (int L = 0; L <= Lend; ++L) {
-            bar_sync(BAR_VW, NVW * 32);  // iteration L-1 done by every vertical thread
-            if (warp == 0 && L + PF <= Lend) issue(L + PF);
-            mbar_wait(&full[sL], ((L + 1) / NSB) & 1);
-            const bool emit = L >= Lf;
-            const int buf = chunk & 1;
-            if (emit) bar_sync(BAR_EMPTY0 + buf, NTH);
-            if (active) {
-                const unsigned char* lead = rbase + (size_t)sL * (B * RP);
-                unsigned char* vb = vt + (size_t)buf * NGC * VTG * ESZ;
-                // store a finished group of GR rows (m0 .. m0+GR-1) of this thread's 2 columns
-                uint32_t grp[GR];
-                auto flush = [&](int m0) {
-                    unsigned char* rowg = vb + (m0 / GR) * VTG * ESZ;
-                    if constexpr (sz == 1) {
-                        if (voff0 >= 0)
-                            *reinterpret_cast<uint2*>(rowg + voff0) =
-                                make_uint2(prmt(grp[0], grp[2], 0x5410), prmt(grp[1], grp[3], 0x5410));
-                        if (voff1 >= 0)
-                            *reinterpret_cast<uint2*>(rowg + voff1) =
-                                make_uint2(prmt(grp[0], grp[2], 0x7632), prmt(grp[1], grp[3], 0x7632));
-                    } else {
-                        if (voff0 >= 0) *reinterpret_cast<uint32_t*>(rowg + voff0) = prmt(grp[0], grp[1], 0x5410);
-                        if (voff1 >= 0) *reinterpret_cast<uint32_t*>(rowg + voff1) = prmt(grp[0], grp[1], 0x7632);
-                    }
-                };
-                if constexpr (VDIRECT) {
-                    constexpr int WD = VB;
-                    uint32_t X[B + WD - 1];
-                    const unsigned char* prev = rbase + (size_t)sL1 * (B * RP);
-#pragma unroll
-                    for (int k = 0; k < WD - 1; ++k) X[k] = ldw(prev + (B - (WD - 1) + k) * RP);
-#pragma unroll
-                    for (int m = 0; m < B; ++m) X[WD - 1 + m] = ldw(lead + m * RP);
-                    if (emit) {
-#pragma unroll
-                        for (int m = 0; m < B; ++m) {
-                            uint32_t o;
-                            if constexpr (WD == 1) o = X[m];
-                            else if constexpr (WD == 3) o = op3(X[m], X[m + 1], X[m + 2]);
-                            else if constexpr (WD == 5) o = op3(op3(X[m], X[m + 1], X[m + 2]), X[m + 3], X[m + 4]);
-                            else o = op3(op3(X[m], X[m + 1], X[m + 2]), op3(X[m + 3], X[m + 4], X[m + 5]), X[m + 6]);
-                            grp[m % GR] = o;
-                            if (m % GR == GR - 1) flush(m - (GR - 1));
-                        }
-                    }
-                } else {
-                    uint32_t P[B];
-                    P[0] = ldw(lead);
-#pragma unroll
-                    for (int m = 1; m < B; ++m) P[m] = op2(P[m - 1], ldw(lead + m * RP));
-                    if (emit) {
-                        // gap = tail r rows of block L-q + whole blocks L-q+1 .. L-1
-                        const unsigned char* tb = rbase + (size_t)sQ * (B * RP);
-                        uint32_t gap = IDV;
-                        for (int i = 0; i < r; ++i) gap = op2(gap, ldw(tb + (B - r + i) * RP));
-#pragma unroll
-                        for (int k = 0; k < QMAX - 1; ++k)
-                            if (k < q - 1) gap = op2(gap, M[k]);
-                        // trailing run rows oL + m: block L-q-1 row B-r+m (m < r), block L-q row m-r
-                        const unsigned char* ta = rbase + (size_t)sQ1 * (B * RP) + (B - r) * RP;
-                        const unsigned char* tbb = tb - r * RP;
-                        uint32_t acc = gap;
-#pragma unroll
-                        for (int m = B - 1; m >= 0; --m) {
-                            acc = op2(acc, ldw((m < r ? ta : tbb) + m * RP));
-                            grp[m % GR] = op2(acc, P[m]);
-                            if (m % GR == 0) flush(m);
-                        }
-                    }
-#pragma unroll
-                    for (int k = QMAX - 1; k > 0; --k) M[k] = M[k - 1];
-                    M[0] = P[B - 1];
-                }
-            }
-            if (emit) {
-                bar_arrive(BAR_FULL0 + buf, NTH);
-                ++chunk;
-            }
+        // consumed block stream: slot/parity of the current block and of blocks -1, -q, -q-1
+        int seq = 0, sL = 0, ph = 0;
+        int sL1 = NSB - 1, sQ = ((-q) % NSB + NSB) % NSB, sQ1 = ((-q - 1) % NSB + NSB) % NSB;
+        auto advance = [&]() {
+            ++seq;
             sL1 = sL;
             sL = sL + 1 == NSB ? 0 : sL + 1;
+            ph ^= sL == 0;
             sQ1 = sQ;
             sQ = sQ + 1 == NSB ? 0 : sQ + 1;
+        };
+        int chunk = 0;
+        for (int n = 0; item_at(n) < nitems; ++n) {
+            const Item it = make_item<T>(p, item_at(n), nstrips, nrowb, B, w1, s);
+            // thread t owns image columns xs_col + 2t, +1 as one u16x2 word (u8 unpacked on load)
+            const int t = tid;
+            const bool active = t < it.nwv;
+            int load_off = 0;
+            uint32_t nib = 0;
+            bool fix = false;
+            col_fix<T>(it.xs_col + 2 * (active ? t : 0), p.W, p.cmode, it.xs_col, load_off, nib, fix);
+            const uint32_t selU =
+                sz == 1 ? ((nib & 0xF) | (5u << 4) | (((nib >> 4) & 0xF) << 8) | (5u << 12)) : nib;
+            const uint32_t Z = bv;
+            int voff0, voff1;
+            {
+                const int pos0 = 2 * t - it.off, pos1 = pos0 + 1;
+                voff0 = (active && pos0 >= 0 && pos0 < 8 * H::NCH) ? ((pos0 & 7) * NCHP + (pos0 >> 3)) * ESZ : -1;
+                voff1 = (active && pos1 >= 0 && pos1 < 8 * H::NCH) ? ((pos1 & 7) * NCHP + (pos1 >> 3)) * ESZ : -1;
+            }
+            auto ldw = [&](const unsigned char* a) -> uint32_t {
+                if constexpr (sz == 1) {
+                    const uint32_t raw = *reinterpret_cast<const uint16_t*>(a);
+                    return prmt(raw, Z, selU);
+                } else {
+                    const uint32_t raw = *reinterpret_cast<const uint32_t*>(a);
+                    return fix ? prmt(raw, Z, selU) : raw;
+                }
+            };
+            const unsigned char* rbase = ring + load_off;
+            auto sbase = [&](int slot) { return rbase + (size_t)slot * (B * RP); };
+
+            // block -1 of this item: never a leading block, wait for it before its trailing use
+            // producer stays exactly PF blocks ahead: consuming seq g issues seq g + PF (the
+            // prologue covered 0..PF), whose slot held seq g + PF - NSB = g - q - 2: dead.
+            bar_sync(BAR_VW, NVW * 32);
+            if (warp == 0 && seq > 0) issue_next();
+            mbar_wait(&full[sL], (uint32_t)ph);
+            advance();
+
+            uint32_t M[QMAX];
+#pragma unroll
+            for (int k = 0; k < QMAX; ++k) M[k] = IDV;
+            for (int L = 0; L <= it.Lend; ++L, advance()) {
+                if (warp == 0 && L < 60 && n == 0) RM_TRACE(L * 8 + 0);
+                bar_sync(BAR_VW, NVW * 32);  // iteration L-1 done by every vertical thread
+                if (warp == 0) issue_next();
+                if (warp == 0 && L < 60 && n == 0) RM_TRACE(L * 8 + 1);
+                mbar_wait(&full[sL], (uint32_t)ph);
+                if (warp == 0 && L < 60 && n == 0) RM_TRACE(L * 8 + 2);
+                const bool emit = L >= it.Lf;
+                const int buf = chunk & 1;
+                if (emit) bar_sync(BAR_EMPTY0 + buf, NTH);
+                if (warp == 0 && L < 60 && n == 0) RM_TRACE(L * 8 + 3);
+                if (active) {
+                    const unsigned char* lead = sbase(sL);
+                    unsigned char* vb = vt + (size_t)buf * NGC * VTG * ESZ;
+                    uint32_t grp[GR];
+                    auto flush = [&](int m0) {
+                        unsigned char* rowg = vb + (m0 / GR) * VTG * ESZ;
+                        if constexpr (sz == 1) {
+                            if (voff0 >= 0)
+                                *reinterpret_cast<uint2*>(rowg + voff0) =
+                                    make_uint2(prmt(grp[0], grp[2], 0x5410), prmt(grp[1], grp[3], 0x5410));
+                            if (voff1 >= 0)
+                                *reinterpret_cast<uint2*>(rowg + voff1) =
+                                    make_uint2(prmt(grp[0], grp[2], 0x7632), prmt(grp[1], grp[3], 0x7632));
+                        } else {
+                            if (voff0 >= 0) *reinterpret_cast<uint32_t*>(rowg + voff0) = prmt(grp[0], grp[1], 0x5410);
+                            if (voff1 >= 0) *reinterpret_cast<uint32_t*>(rowg + voff1) = prmt(grp[0], grp[1], 0x7632);
+                        }
+                    };
+                    if constexpr (VDIRECT) {
+                        constexpr int WD = VB;
+                        uint32_t X[B + WD - 1];
+                        const unsigned char* prev = sbase(sL1);
+#pragma unroll
+                        for (int k = 0; k < WD - 1; ++k) X[k] = ldw(prev + (B - (WD - 1) + k) * RP);
+#pragma unroll
+                        for (int m = 0; m < B; ++m) X[WD - 1 + m] = ldw(lead + m * RP);
+                        if (emit) {
+#pragma unroll
+                            for (int m = 0; m < B; ++m) {
+                                uint32_t o;
+                                if constexpr (WD == 1) o = X[m];
+                                else if constexpr (WD == 3) o = op3(X[m], X[m + 1], X[m + 2]);
+                                else if constexpr (WD == 5) o = op3(op3(X[m], X[m + 1], X[m + 2]), X[m + 3], X[m + 4]);
+                                else o = op3(op3(X[m], X[m + 1], X[m + 2]), op3(X[m + 3], X[m + 4], X[m + 5]), X[m + 6]);
+                                grp[m % GR] = o;
+                                if (m % GR == GR - 1) flush(m - (GR - 1));
+                            }
+                        }
+                    } else {
+                        uint32_t P[B];
+                        P[0] = ldw(lead);
+#pragma unroll
+                        for (int m = 1; m < B; ++m) P[m] = op2(P[m - 1], ldw(lead + m * RP));
+                        if (emit) {
+                            // gap = tail r rows of block L-q + whole blocks L-q+1 .. L-1 (tree-reduced)
+                            const unsigned char* tb = sbase(sQ);  // block L-q
+                            const unsigned char* tt = tb + (B - r) * RP;
+                            uint32_t v[B + QMAX];
+#pragma unroll
+                            for (int i = 0; i < B - 1; ++i) v[i] = i < r ? ldw(tt + i * RP) : IDV;
+#pragma unroll
+                            for (int k = 0; k < QMAX - 1; ++k) v[B - 1 + k] = k < q - 1 ? M[k] : IDV;
+                            constexpr int NV = B - 1 + QMAX - 1;
+                            uint32_t gap = IDV;
+#pragma unroll
+                            for (int i = 0; i < NV; i += 3) {
+                                const uint32_t x = v[i], y = i + 1 < NV ? v[i + 1] : IDV, z = i + 2 < NV ? v[i + 2] : IDV;
+                                v[i / 3] = op3(x, y, z);
+                            }
+#pragma unroll
+                            for (int i = 0; i < (NV + 2) / 3; i += 3) {
+                                const int nv2 = (NV + 2) / 3;
+                                const uint32_t x = v[i], y = i + 1 < nv2 ? v[i + 1] : IDV, z = i + 2 < nv2 ? v[i + 2] : IDV;
+                                gap = op3(gap, op3(x, y, z), IDV);
+                            }
+                            // trailing run rows oL + m: block L-q-1 row B-r+m (m < r), block L-q row m-r
+                            const unsigned char* ta = sbase(sQ1) + (B - r) * RP;
+                            const unsigned char* tbb = tb - r * RP;
+                            uint32_t acc = gap;
+#pragma unroll
+                            for (int m = B - 1; m >= 0; --m) {
+                                acc = op2(acc, ldw((m < r ? ta : tbb) + m * RP));
+                                grp[m % GR] = op2(acc, P[m]);
+                                if (m % GR == 0) flush(m);
+                            }
+                        }
+#pragma unroll
+                        for (int k = QMAX - 1; k > 0; --k) M[k] = M[k - 1];
+                        M[0] = P[B - 1];
+                    }
+                }
+                if (warp == 0 && L < 60 && n == 0) RM_TRACE(L * 8 + 4);
+                if (emit) {
+                    bar_arrive(BAR_FULL0 + buf, NTH);
+                    ++chunk;
+                }
+            }
         }
         // balance the horizontal side's extra releases so every barrier generation completes
         bar_sync(BAR_EMPTY0 + (chunk & 1), NTH);
@@ -422,7 +534,6 @@ morph_stream_kernel(StreamParams p) {
         unsigned char* scr = hs + (size_t)(hw * SUBG + sub) * (VTG + NCHP) * ESZ;  // P scratch, then M
         unsigned char* msc = scr + (size_t)VTG * ESZ;
         const int q8 = w1x >> 3, r8 = w1x & 7;
-        int chunk = 0;
         auto ld8 = [&](const unsigned char* a) -> LW<T> {
             LW<T> v;
             if constexpr (sz == 1) {
@@ -438,129 +549,147 @@ morph_stream_kernel(StreamParams p) {
             if constexpr (sz == 1) *reinterpret_cast<uint2*>(a) = make_uint2(v.a, v.b);
             else *reinterpret_cast<uint32_t*>(a) = v.a;
         };
-        for (int L = Lf; L <= Lend; ++L, ++chunk) {
-            const int buf = chunk & 1;
-            bar_sync(BAR_FULL0 + buf, NTH);
-            const int oL = s + L * B - w1;
-            const unsigned char* vb = vt + (size_t)buf * NGC * VTG * ESZ;
-            for (int g0 = hw * SUBG; g0 < NGC; g0 += NHW * SUBG) {
-                const int g = g0 + sub;
-                const int o_g = oL + g * GR;
-                const bool live = g < NGC && o_g + GR - 1 >= 0 && o_g < rh;
-                const unsigned char* rowg = vb + (size_t)(g < NGC ? g : 0) * VTG * ESZ;
-                // emit GR output columns (a..a+GR-1) of rows g*GR.. into the output tile
-                auto emit4 = [&](int a, LW<T> c0, LW<T> c1, LW<T> c2, LW<T> c3) {
-                    unsigned char* po = outt + (size_t)(g * GR) * OUTP + (size_t)a * sz;
-                    if constexpr (sz == 1) {
-                        const uint32_t a01 = prmt(c0.a, c1.a, 0x6240), a23 = prmt(c2.a, c3.a, 0x6240);
-                        const uint32_t b01 = prmt(c0.b, c1.b, 0x6240), b23 = prmt(c2.b, c3.b, 0x6240);
-                        *reinterpret_cast<uint32_t*>(po) = prmt(a01, a23, 0x5410);
-                        *reinterpret_cast<uint32_t*>(po + OUTP) = prmt(b01, b23, 0x5410);
-                        *reinterpret_cast<uint32_t*>(po + 2 * OUTP) = prmt(a01, a23, 0x7632);
-                        *reinterpret_cast<uint32_t*>(po + 3 * OUTP) = prmt(b01, b23, 0x7632);
-                    } else {  // u16: two columns per call (c2, c3 unused)
-                        *reinterpret_cast<uint32_t*>(po) = prmt(c0.a, c1.a, 0x5410);
-                        *reinterpret_cast<uint32_t*>(po + OUTP) = prmt(c0.a, c1.a, 0x7632);
-                    }
-                };
-                auto emit8 = [&](const LW<T> (&o)[8]) {
-#pragma unroll
-                    for (int j = 0; j < 8; j += GR) {
-                        if constexpr (GR == 4) emit4(8 * lam + j, o[j], o[j + 1], o[j + 2], o[j + 3]);
-                        else emit4(8 * lam + j, o[j], o[j + 1], o[j], o[j]);
-                    }
-                };
-                if constexpr (HB <= 7) {
-                    // direct window: lane owns 8 output columns; position 8*lam + i, i < 8 + WD - 1
-                    constexpr int WD = HB;
-                    LW<T> X[8 + WD - 1];
-                    const unsigned char* b0 = rowg + lam * ESZ;
-#pragma unroll
-                    for (int i = 0; i < 8 + WD - 1; ++i)
-                        X[i] = ld8(b0 + ((i & 7) * NCHP + (i >> 3)) * ESZ);
-                    LW<T> o[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        if constexpr (WD == 1) o[j] = X[j];
-                        else if constexpr (WD == 3) o[j] = lop3<MODE>(X[j], X[j + 1], X[j + 2]);
-                        else if constexpr (WD == 5) o[j] = lop3<MODE>(lop3<MODE>(X[j], X[j + 1], X[j + 2]), X[j + 3], X[j + 4]);
-                        else o[j] = lop3<MODE>(lop3<MODE>(X[j], X[j + 1], X[j + 2]), lop3<MODE>(X[j + 3], X[j + 4], X[j + 5]), X[j + 6]);
-                    }
-                    if (live) emit8(o);
-                } else {
-                    // lane-chunk van Herk over 8-column chunks: prefix -> scratch, suffix in registers
-                    const int nch = (TW + w1x + 7) >> 3;
-                    LW<T> S[8];
-                    for (int k = lam; k < nch; k += LPG) {
-                        LW<T> x[8];
-                        const unsigned char* b0 = rowg + k * ESZ;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) x[j] = ld8(b0 + j * NCHP * ESZ);
-                        LW<T> pre = x[0];
-                        unsigned char* pb = scr + k * ESZ;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            if (j) pre = lop<MODE>(pre, x[j]);
-                            st8(pb + j * NCHP * ESZ, pre);
+        int chunk = 0;
+        for (int n = 0; item_at(n) < nitems; ++n) {
+            const Item it = make_item<T>(p, item_at(n), nstrips, nrowb, B, w1, s);
+            uint8_t* dst = p.dst + (size_t)it.b * p.dimg;
+            for (int L = it.Lf; L <= it.Lend; ++L, ++chunk) {
+                const int buf = chunk & 1;
+                if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 0);
+                bar_sync(BAR_FULL0 + buf, NTH);
+                if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 1);
+                const int oL = s + L * B - w1;
+                const unsigned char* vb = vt + (size_t)buf * NGC * VTG * ESZ;
+                for (int g0 = hw * SUBG; g0 < NGC; g0 += NHW * SUBG) {
+                    const int g = g0 + sub;
+                    const int o_g = oL + g * GR;
+                    const bool live = g < NGC && o_g + GR - 1 >= 0 && o_g < it.rh;
+                    const unsigned char* rowg = vb + (size_t)(g < NGC ? g : 0) * VTG * ESZ;
+                    auto emit4 = [&](int a, LW<T> c0, LW<T> c1, LW<T> c2, LW<T> c3) {
+                        unsigned char* po = outt + (size_t)(g * GR) * OUTP + (size_t)a * sz;
+                        if constexpr (sz == 1) {
+                            const uint32_t a01 = prmt(c0.a, c1.a, 0x6240), a23 = prmt(c2.a, c3.a, 0x6240);
+                            const uint32_t b01 = prmt(c0.b, c1.b, 0x6240), b23 = prmt(c2.b, c3.b, 0x6240);
+                            *reinterpret_cast<uint32_t*>(po) = prmt(a01, a23, 0x5410);
+                            *reinterpret_cast<uint32_t*>(po + OUTP) = prmt(b01, b23, 0x5410);
+                            *reinterpret_cast<uint32_t*>(po + 2 * OUTP) = prmt(a01, a23, 0x7632);
+                            *reinterpret_cast<uint32_t*>(po + 3 * OUTP) = prmt(b01, b23, 0x7632);
+                        } else {  // u16: two columns per call (c2, c3 unused)
+                            *reinterpret_cast<uint32_t*>(po) = prmt(c0.a, c1.a, 0x5410);
+                            *reinterpret_cast<uint32_t*>(po + OUTP) = prmt(c0.a, c1.a, 0x7632);
                         }
-                        st8(msc + k * ESZ, pre);
-                        if (k == lam) {
-                            S[7] = x[7];
+                    };
+                    auto emit8 = [&](const LW<T> (&o)[8]) {
 #pragma unroll
-                            for (int j = 6; j >= 0; --j) S[j] = lop<MODE>(S[j + 1], x[j]);
+                        for (int j = 0; j < 8; j += GR) {
+                            if constexpr (GR == 4) emit4(8 * lam + j, o[j], o[j + 1], o[j + 2], o[j + 3]);
+                            else emit4(8 * lam + j, o[j], o[j + 1], o[j], o[j]);
                         }
-                    }
-                    __syncwarp();
-                    {
-                        const int k = lam;
-                        LW<T> Fa = lid<T, MODE>();
-                        for (int i = 1; i < q8; ++i) Fa = lop<MODE>(Fa, ld8(msc + (k + i) * ESZ));
-                        const LW<T> Fb = lop<MODE>(Fa, ld8(msc + (k + q8) * ESZ));
-                        // P at position 8k + j + w1x: chunk k+q8 (+1), index (j + r8) & 7
-                        const unsigned char* pa = scr + (r8 * NCHP + k + q8) * ESZ;
-                        const unsigned char* pbb = scr + ((r8 - 8) * NCHP + k + q8 + 1) * ESZ;
+                    };
+                    if constexpr (HB <= 7) {
+                        constexpr int WD = HB;
+                        LW<T> X[8 + WD - 1];
+                        const unsigned char* b0 = rowg + lam * ESZ;
+#pragma unroll
+                        for (int i = 0; i < 8 + WD - 1; ++i) X[i] = ld8(b0 + ((i & 7) * NCHP + (i >> 3)) * ESZ);
                         LW<T> o[8];
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const bool lo = j < 8 - r8;
-                            o[j] = lop3<MODE>(S[j], lo ? Fa : Fb, ld8((lo ? pa : pbb) + j * NCHP * ESZ));
+                            if constexpr (WD == 1) o[j] = X[j];
+                            else if constexpr (WD == 3) o[j] = lop3<MODE>(X[j], X[j + 1], X[j + 2]);
+                            else if constexpr (WD == 5) o[j] = lop3<MODE>(lop3<MODE>(X[j], X[j + 1], X[j + 2]), X[j + 3], X[j + 4]);
+                            else o[j] = lop3<MODE>(lop3<MODE>(X[j], X[j + 1], X[j + 2]), lop3<MODE>(X[j + 3], X[j + 4], X[j + 5]), X[j + 6]);
                         }
                         if (live) emit8(o);
+                    } else {
+                        const int nch = (TW + w1x + 7) >> 3;
+                        LW<T> S[8];
+                        for (int k = lam; k < nch; k += LPG) {
+                            LW<T> x[8];
+                            const unsigned char* b0 = rowg + k * ESZ;
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) x[j] = ld8(b0 + j * NCHP * ESZ);
+                            LW<T> pre = x[0];
+                            unsigned char* pb = scr + k * ESZ;
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                if (j) pre = lop<MODE>(pre, x[j]);
+                                st8(pb + j * NCHP * ESZ, pre);
+                            }
+                            st8(msc + k * ESZ, pre);
+                            if (k == lam) {
+                                S[7] = x[7];
+#pragma unroll
+                                for (int j = 6; j >= 0; --j) S[j] = lop<MODE>(S[j + 1], x[j]);
+                            }
+                        }
+                        __syncwarp();
+                        {
+                            const int k = lam;
+                            // chunk minima strictly between (k, k+q8[+1]): tree of predicated loads
+                            constexpr int QM8 = H::GXMAX / 4 + 1;
+                            LW<T> mv[QM8 + 2];
+#pragma unroll
+                            for (int i = 0; i < QM8 + 2; ++i) mv[i] = lid<T, MODE>();
+#pragma unroll
+                            for (int i = 1; i < QM8; ++i)
+                                if (i < q8) mv[i - 1] = ld8(msc + (k + i) * ESZ);
+                            LW<T> Fa = lid<T, MODE>();
+#pragma unroll
+                            for (int i = 0; i < QM8; i += 3) Fa = lop<MODE>(Fa, lop3<MODE>(mv[i], mv[i + 1], mv[i + 2]));
+                            const LW<T> Fb = lop<MODE>(Fa, ld8(msc + (k + q8) * ESZ));
+                            const unsigned char* pa = scr + (r8 * NCHP + k + q8) * ESZ;
+                            const unsigned char* pbb = scr + ((r8 - 8) * NCHP + k + q8 + 1) * ESZ;
+                            LW<T> o[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const bool lo = j < 8 - r8;
+                                o[j] = lop3<MODE>(S[j], lo ? Fa : Fb, ld8((lo ? pa : pbb) + j * NCHP * ESZ));
+                            }
+                            if (live) emit8(o);
+                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
                 }
-            }
-            bar_arrive(BAR_EMPTY0 + buf, NTH);
-            bar_sync(BAR_HW, NHW * 32);
-            // store the valid rows of the chunk
-            {
-                const int htid = tid - NVW * 32;  // horizontal thread index
-                const int cols = min(TW, p.W - x0);
-                const int row_bytes = cols * sz;
-                const bool vec = (((uintptr_t)dst | p.dp) & 15) == 0 && cols == TW;
-                const int rlo = max(0, -oL), rhi = min(B, rh - oL);
-                if (vec) {
-                    constexpr int CPR = TW * sz / 16;
-                    for (int i = rlo * CPR + htid; i < rhi * CPR; i += NHW * 32) {
-                        const int rr = i / CPR, ch = i % CPR;
-                        const uint4 v = *reinterpret_cast<const uint4*>(outt + (size_t)rr * OUTP + ch * 16);
-                        *reinterpret_cast<uint4*>(dst + (size_t)(y0 + oL + rr) * p.dp + (size_t)x0 * sz + ch * 16) = v;
-                    }
-                } else {
-                    for (int i = rlo * row_bytes + htid; i < rhi * row_bytes; i += NHW * 32) {
-                        const int rr = i / row_bytes, b = i % row_bytes;
-                        dst[(size_t)(y0 + oL + rr) * p.dp + (size_t)x0 * sz + b] = outt[(size_t)rr * OUTP + b];
+                if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 2);
+                bar_arrive(BAR_EMPTY0 + buf, NTH);
+                bar_sync(BAR_HW, NHW * 32);
+                if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 3);
+                {
+                    const int htid = tid - NVW * 32;  // horizontal thread index
+                    const int cols = min(TW, p.W - it.x0);
+                    const int row_bytes = cols * sz;
+                    const bool vec = (((uintptr_t)dst | p.dp) & 15) == 0 && cols == TW;
+                    const int rlo = max(0, -oL), rhi = min(B, it.rh - oL);
+                    if (vec) {
+                        constexpr int CPR = TW * sz / 16;
+                        for (int i = rlo * CPR + htid; i < rhi * CPR; i += NHW * 32) {
+                            const int rr = i / CPR, ch = i % CPR;
+                            const uint4 v = *reinterpret_cast<const uint4*>(outt + (size_t)rr * OUTP + ch * 16);
+                            *reinterpret_cast<uint4*>(dst + (size_t)(it.y0 + oL + rr) * p.dp + (size_t)it.x0 * sz + ch * 16) = v;
+                        }
+                    } else {
+                        for (int i = rlo * row_bytes + htid; i < rhi * row_bytes; i += NHW * 32) {
+                            const int rr = i / row_bytes, b = i % row_bytes;
+                            dst[(size_t)(it.y0 + oL + rr) * p.dp + (size_t)it.x0 * sz + b] = outt[(size_t)rr * OUTP + b];
+                        }
                     }
                 }
+                bar_sync(BAR_HW, NHW * 32);
+                if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 4);
             }
-            bar_sync(BAR_HW, NHW * 32);
         }
     }
 }
 
 // ---- host launch ------------------------------------------------------------------------------
+extern long long* g_trace;   // debug timeline buffer (device), set by rmgpu_debug_trace
+extern int g_trace_cta;
+// Encodes the 3-D tensor map {words, rows, images} of the job's valid input rows (host).
+bool encode_input_map(const MorphJob& j, int box_words, int box_rows, CUtensorMap* map);
+
 template <typename T, int MODE, int VB, int HB>
-cudaError_t launch_stream_variant(const MorphJob& j, int rh, int B, int q) {
+cudaError_t launch_stream_variant(const MorphJob& j, int rh, int B, int q, int pf) {
     using G = SG<T>;
     StreamParams p;
     p.src = static_cast<const uint8_t*>(j.src);
@@ -578,12 +707,26 @@ cudaError_t launch_stream_variant(const MorphJob& j, int rh, int B, int q) {
     p.simg = j.simg;
     p.dimg = j.dimg;
     p.rh = rh;
-    const Plan pl = make_plan<T, HB>(B, q);
+    p.pf = pf;
+    p.trace = g_trace;
+    p.trace_cta = g_trace_cta;
+    CUtensorMap map;
+    p.use_tma = encode_input_map(j, HG<T, HB>::RP / 4, B, &map) ? 1 : 0;
+    const Plan pl = make_plan<T, HB>(B, q, pf);
     auto kern = morph_stream_kernel<T, MODE, VB, HB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
     if (e != cudaSuccess) return e;
-    dim3 grid(cdiv(j.W, G::TW), cdiv(j.H, rh), j.batch);
-    kern<<<grid, HG<T, HB>::NTH, pl.total, j.stream>>>(p);
+    const long items = (long)cdiv(j.W, G::TW) * cdiv(j.H, rh) * j.batch;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, KG<T, VB, HB>::NTH, pl.total);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long ctas = std::max(1L, std::min(items, (long)sms * std::max(1, occ)));
+    dim3 grid((unsigned)ctas, 1, 1);
+    p.batch = j.batch;
+    kern<<<grid, KG<T, VB, HB>::NTH, pl.total, j.stream>>>(p, map);
     count_launch();
     return cudaGetLastError();
 }
@@ -592,10 +735,10 @@ cudaError_t launch_stream_variant(const MorphJob& j, int rh, int B, int q) {
 #define RM_STREAM_H(X) X(1) X(3) X(5) X(7) X(8) X(9)
 
 template <typename T, int MODE, int VB>
-cudaError_t stream_dispatch_h(const MorphJob& j, int hb, int rh, int B, int q) {
+cudaError_t stream_dispatch_h(const MorphJob& j, int hb, int rh, int B, int q, int pf) {
     switch (hb) {
 #define RM_CASE(H) \
-    case H: return launch_stream_variant<T, MODE, VB, H>(j, rh, B, q);
+    case H: return launch_stream_variant<T, MODE, VB, H>(j, rh, B, q, pf);
         RM_STREAM_H(RM_CASE)
 #undef RM_CASE
     }
@@ -603,10 +746,10 @@ cudaError_t stream_dispatch_h(const MorphJob& j, int hb, int rh, int B, int q) {
 }
 
 template <typename T, int MODE>
-cudaError_t stream_dispatch(const MorphJob& j, int vb, int hb, int rh, int B, int q) {
+cudaError_t stream_dispatch(const MorphJob& j, int vb, int hb, int rh, int B, int q, int pf) {
     switch (vb) {
 #define RM_CASE(V) \
-    case V: return stream_dispatch_h<T, MODE, V>(j, hb, rh, B, q);
+    case V: return stream_dispatch_h<T, MODE, V>(j, hb, rh, B, q, pf);
         RM_STREAM_V(RM_CASE)
 #undef RM_CASE
     }
@@ -620,14 +763,26 @@ inline int stream_gxmax(int elem, int hb) {
 }
 
 template <typename T>
-inline int stream_smem(int hb, int B, int q) {
+inline int stream_smem(int hb, int B, int q, int pf) {
     switch (hb) {
-    case 1: return make_plan<T, 1>(B, q).total;
-    case 3: return make_plan<T, 3>(B, q).total;
-    case 5: return make_plan<T, 5>(B, q).total;
-    case 7: return make_plan<T, 7>(B, q).total;
-    case 8: return make_plan<T, 8>(B, q).total;
-    default: return make_plan<T, 9>(B, q).total;
+    case 1: return make_plan<T, 1>(B, q, pf).total;
+    case 3: return make_plan<T, 3>(B, q, pf).total;
+    case 5: return make_plan<T, 5>(B, q, pf).total;
+    case 7: return make_plan<T, 7>(B, q, pf).total;
+    case 8: return make_plan<T, 8>(B, q, pf).total;
+    default: return make_plan<T, 9>(B, q, pf).total;
+    }
+}
+
+template <typename T>
+inline int stream_ring_row(int hb) {
+    switch (hb) {
+    case 1: return HG<T, 1>::RP;
+    case 3: return HG<T, 3>::RP;
+    case 5: return HG<T, 5>::RP;
+    case 7: return HG<T, 7>::RP;
+    case 8: return HG<T, 8>::RP;
+    default: return HG<T, 9>::RP;
     }
 }
 

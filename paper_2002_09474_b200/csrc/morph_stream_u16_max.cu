@@ -3,8 +3,8 @@
 
 namespace rmgpu {
 namespace stream {
-cudaError_t dispatch_u16_max(const MorphJob& j, int vb, int hb, int rh, int B, int q) {
-    return stream_dispatch<uint16_t, MODE_MAX>(j, vb, hb, rh, B, q);
+cudaError_t dispatch_u16_max(const MorphJob& j, int vb, int hb, int rh, int B, int q, int pf) {
+    return stream_dispatch<uint16_t, MODE_MAX>(j, vb, hb, rh, B, q, pf);
 }
 }  // namespace stream
 }  // namespace rmgpu

@@ -3,8 +3,8 @@
 
 namespace rmgpu {
 namespace stream {
-cudaError_t dispatch_u8_min(const MorphJob& j, int vb, int hb, int rh, int B, int q) {
-    return stream_dispatch<uint8_t, MODE_MIN>(j, vb, hb, rh, B, q);
+cudaError_t dispatch_u8_min(const MorphJob& j, int vb, int hb, int rh, int B, int q, int pf) {
+    return stream_dispatch<uint8_t, MODE_MIN>(j, vb, hb, rh, B, q, pf);
 }
 }  // namespace stream
 }  // namespace rmgpu

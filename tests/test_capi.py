@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared(header: str) -> set[str]:
     text = open(os.path.join(ROOT, "include", header)).read()
-    return set(re.findall(r"^\s*(?:int|const char\*|unsigned long long)\s+(rmgpu_\w+)\s*\(", text, re.M))
+    return set(re.findall(r"^\s*(?:int|void|const char\*|unsigned long long)\s+(rmgpu_\w+)\s*\(", text, re.M))
 
 
 def test_library_exports_every_declared_symbol():
