@@ -159,6 +159,22 @@ bool encode_input_map(const MorphJob& j, int box_words, int box_rows, CUtensorMa
     return r == CUDA_SUCCESS;
 }
 
+bool encode_output_map(const MorphJob& j, int box_bytes, int box_rows, CUtensorMap* map) {
+    memset(map, 0, sizeof(*map));
+    if (getenv("RMGPU_NO_TMA")) return false;
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    if (j.dp % 16 || (j.batch > 1 && j.dimg % 16) || (reinterpret_cast<uintptr_t>(j.dst) & 15)) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)j.W * j.elem, (cuuint64_t)j.H, (cuuint64_t)std::max(1, j.batch)};
+    cuuint64_t strides[2] = {j.dp, j.batch > 1 ? j.dimg : j.dp * (cuuint64_t)j.H};
+    cuuint32_t box[3] = {(cuuint32_t)box_bytes, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, j.dst, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 void set_trace(long long* buf, int cta) {
     g_trace = buf;
     g_trace_cta = cta;

@@ -114,6 +114,16 @@ __device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* map, int x
         "l"(map), "r"(x), "r"(y), "r"(z), "r"(saddr(bar))
         : "memory");
 }
+// TMA tensor store of a box {TW*sz bytes, B rows} from shared memory (3-D map: bytes, rows, images).
+__device__ __forceinline__ void tma_store_box(const CUtensorMap* map, int x, int y, int z, const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map),
+                 "r"(x), "r"(y), "r"(z), "r"(saddr(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
@@ -136,14 +146,20 @@ struct StreamParams {
     long long* trace;     // debug timeline (nullptr normally): CTA (trace_cta) records clock64 stamps
     int trace_cta;
     int use_tma;          // interior blocks through one 2-D tensor copy (map rows start at row_lo)
+    int use_tma_out;      // full output chunks through one TMA tensor store
     int batch;            // images
 };
 
+#ifdef RMGPU_TRACE
 #define RM_TRACE(slot)                                                                                   \
     do {                                                                                                 \
-        if (p.trace && blockIdx.x == (unsigned)p.trace_cta && (threadIdx.x & 31) == 0) \
-            p.trace[(slot)] = clock64();                                                                 \
+        if (p.trace && blockIdx.x == (unsigned)p.trace_cta && (threadIdx.x & 31) == 0) p.trace[(slot)] = clock64(); \
     } while (0)
+#else
+#define RM_TRACE(slot) \
+    do {               \
+    } while (0)
+#endif
 
 // Compile-time geometry of one horizontal class HB: 1/3/5/7 = direct window (gx = (HB-1)/2),
 // 8 / 9 = lane-chunk block algorithm for gx up to GXMAX (small / large halo).
@@ -178,8 +194,9 @@ __host__ __device__ inline Plan make_plan(int B, int q, int PF) {
     o += 2 * (B / G::GR) * H::VTG * G::ESZ;
     p.off_hs = o;
     if (HB > 7) o += nhw_of(B) * (32 / H::LPG) * (H::VTG + H::NCHP) * G::ESZ;
+    o = (o + 127) / 128 * 128;
     p.off_out = o;
-    o += B * (G::TW * (int)sizeof(T) + 16);
+    o += 2 * B * G::TW * (int)sizeof(T);
     p.total = o;
     return p;
 }
@@ -266,7 +283,8 @@ __device__ __forceinline__ uint32_t tree_min(uint32_t a, uint32_t b, uint32_t c)
 
 template <typename T, int MODE, int VB, int HB>
 __global__ void __launch_bounds__(KG<T, VB, HB>::NTH)
-morph_stream_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tmap) {
+morph_stream_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tmap,
+                    const __grid_constant__ CUtensorMap omap) {
     using G = SG<T>;
     using H = HG<T, HB>;
     constexpr int GR = G::GR, TW = G::TW, ESZ = G::ESZ;
@@ -274,7 +292,7 @@ morph_stream_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tm
     constexpr bool VDIRECT = VB <= 7;
     constexpr int B = VDIRECT ? VCH : VB;
     constexpr int NGC = B / GR;          // row groups per chunk
-    constexpr int OUTP = TW * sz + 16;
+    constexpr int OUTP = TW * sz;        // output tile row pitch (packed: TMA store box)
     constexpr int RP = H::RP, NCHP = H::NCHP, VTG = H::VTG, LPG = H::LPG;
     constexpr int NVW = KG<T, VB, HB>::NVW, NTH = KG<T, VB, HB>::NTH, NHW = KG<T, VB, HB>::NHW;
     constexpr int SUBG = 32 / LPG;       // row groups per warp pass
@@ -297,7 +315,7 @@ morph_stream_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tm
     unsigned char* ring = smem + pl.off_ring;
     unsigned char* vt = smem + pl.off_vt;
     unsigned char* hs = smem + pl.off_hs;
-    unsigned char* outt = smem + pl.off_out;
+    unsigned char* outbase = smem + pl.off_out;
 
     const uint32_t bv = sz == 1 ? (p.bval & 0xFF) : (p.bval & 0xFFFF);
 
@@ -556,7 +574,10 @@ morph_stream_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tm
             for (int L = it.Lf; L <= it.Lend; ++L, ++chunk) {
                 const int buf = chunk & 1;
                 if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 0);
+                // the previous chunk's TMA store must have finished reading its output buffer
+                if (p.use_tma_out && tid == NVW * 32) bulk_wait_read0();
                 bar_sync(BAR_FULL0 + buf, NTH);
+                unsigned char* outt = outbase + (size_t)buf * B * OUTP;
                 if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 1);
                 const int oL = s + L * B - w1;
                 const unsigned char* vb = vt + (size_t)buf * NGC * VTG * ESZ;
@@ -653,14 +674,23 @@ morph_stream_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tm
                 }
                 if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 2);
                 bar_arrive(BAR_EMPTY0 + buf, NTH);
+                const int rlo = max(0, -oL), rhi = min(B, it.rh - oL);
+                // TMA stores only full chunks of full-width strips: the hardware rounds the right
+                // clip edge to 16 bytes, which would touch the caller's row padding
+                const bool full_chunk = p.use_tma_out && rlo == 0 && rhi == B && it.x0 + TW <= p.W;
+                if (full_chunk) fence_async_smem();  // emits visible to the TMA (async proxy)
                 bar_sync(BAR_HW, NHW * 32);
                 if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 3);
-                {
+                if (full_chunk) {
+                    if (tid == NVW * 32) {
+                        tma_store_box(&omap, it.x0 * sz, it.y0 + oL, it.b, outt);
+                        bulk_commit();
+                    }
+                } else {
                     const int htid = tid - NVW * 32;  // horizontal thread index
                     const int cols = min(TW, p.W - it.x0);
                     const int row_bytes = cols * sz;
                     const bool vec = (((uintptr_t)dst | p.dp) & 15) == 0 && cols == TW;
-                    const int rlo = max(0, -oL), rhi = min(B, it.rh - oL);
                     if (vec) {
                         constexpr int CPR = TW * sz / 16;
                         for (int i = rlo * CPR + htid; i < rhi * CPR; i += NHW * 32) {
@@ -675,10 +705,10 @@ morph_stream_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tm
                         }
                     }
                 }
-                bar_sync(BAR_HW, NHW * 32);
                 if (hw == 0 && L < 60 && n == 0) RM_TRACE(480 + L * 8 + 4);
             }
         }
+        if (p.use_tma_out && tid == NVW * 32) bulk_wait_all();
     }
 }
 
@@ -687,6 +717,8 @@ extern long long* g_trace;   // debug timeline buffer (device), set by rmgpu_deb
 extern int g_trace_cta;
 // Encodes the 3-D tensor map {words, rows, images} of the job's valid input rows (host).
 bool encode_input_map(const MorphJob& j, int box_words, int box_rows, CUtensorMap* map);
+// 3-D byte-granular map {bytes, rows, images} of the output (box = one full chunk of the strip).
+bool encode_output_map(const MorphJob& j, int box_bytes, int box_rows, CUtensorMap* map);
 
 template <typename T, int MODE, int VB, int HB>
 cudaError_t launch_stream_variant(const MorphJob& j, int rh, int B, int q, int pf) {
@@ -712,6 +744,8 @@ cudaError_t launch_stream_variant(const MorphJob& j, int rh, int B, int q, int p
     p.trace_cta = g_trace_cta;
     CUtensorMap map;
     p.use_tma = encode_input_map(j, HG<T, HB>::RP / 4, B, &map) ? 1 : 0;
+    CUtensorMap omap;
+    p.use_tma_out = encode_output_map(j, G::TW * (int)sizeof(T), B, &omap) ? 1 : 0;
     const Plan pl = make_plan<T, HB>(B, q, pf);
     auto kern = morph_stream_kernel<T, MODE, VB, HB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
@@ -726,7 +760,7 @@ cudaError_t launch_stream_variant(const MorphJob& j, int rh, int B, int q, int p
     const long ctas = std::max(1L, std::min(items, (long)sms * std::max(1, occ)));
     dim3 grid((unsigned)ctas, 1, 1);
     p.batch = j.batch;
-    kern<<<grid, KG<T, VB, HB>::NTH, pl.total, j.stream>>>(p, map);
+    kern<<<grid, KG<T, VB, HB>::NTH, pl.total, j.stream>>>(p, map, omap);
     count_launch();
     return cudaGetLastError();
 }
