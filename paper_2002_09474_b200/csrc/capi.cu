@@ -27,10 +27,15 @@ using rmgpu::MorphJob;
 namespace {
 
 thread_local std::string t_last_error;
-// Test hook: RMGPU_DISABLE_STREAM=1 routes around the streaming kernel (exercises the fallbacks).
+// Test / tuning hooks: RMGPU_DISABLE_STREAM=1 routes around the TMA kernels (exercises the
+// fallbacks); RMGPU_KERNEL=stream prefers the warp-specialised kernel over the phase kernel.
 const bool g_disable_stream = [] {
     const char* v = getenv("RMGPU_DISABLE_STREAM");
     return v && v[0] == '1';
+}();
+const bool g_prefer_stream = [] {
+    const char* v = getenv("RMGPU_KERNEL");
+    return v && v[0] == 's';
 }();
 
 int fail(int status, const std::string& msg) {
@@ -117,6 +122,10 @@ int run_single(MorphJob j) {
         return RMGPU_OK;
     }
     cudaError_t e = cudaSuccess;
+    if (!g_disable_stream && !g_prefer_stream && rmgpu::phase::launch(j, &e)) {
+        if (e != cudaSuccess) return cuda_fail(e, "phase morph kernel");
+        return RMGPU_OK;
+    }
     if (!g_disable_stream && rmgpu::stream::launch(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "stream morph kernel");
         return RMGPU_OK;
@@ -345,6 +354,8 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
     j.mode = op == RMGPU_ERODE ? rmgpu::MODE_MIN : op == RMGPU_DILATE ? rmgpu::MODE_MAX : rmgpu::MODE_GRAD;
     if (op == RMGPU_OPEN || op == RMGPU_CLOSE) j.mode = rmgpu::MODE_MIN;
     if (j.gx == 0 && j.gy == 0) return "copy";
+    if (!g_disable_stream && !g_prefer_stream)
+        if (const char* n = rmgpu::phase::plan_name(j)) return n;
     if (!g_disable_stream)
         if (const char* n = rmgpu::stream::plan_name(j)) return n;
     if (const char* n = rmgpu::fast_plan_name(j)) return n;

@@ -48,6 +48,12 @@ const char* plan_name(const MorphJob& j);
 void set_trace(long long* device_buf, int cta);  // debug timeline (tools/trace_stream.py)
 }  // namespace stream
 
+// ---- persistent phase-based fused path (morph_phase.cu), preferred over the streaming one -----
+namespace phase {
+bool launch(const MorphJob& j, cudaError_t* err);
+const char* plan_name(const MorphJob& j);
+}  // namespace phase
+
 // ---- transposes (transpose.cu) ---------------------------------------------------------------
 cudaError_t launch_transpose(const void* src, size_t sp, void* dst, size_t dp, int W, int H,
                              int elem, cudaStream_t s);

@@ -1,0 +1,140 @@
+// morph_phase.cu -- planner for K1/K2 v3, the persistent phase-based fused kernel.
+//
+// Design (B200-first; reference semantics from separable.cpp:130-157, sliding_extrema.cpp,
+// image.cpp:58-66):
+//   * Persistent CTAs (one per resident slot) walk work items = (strip of TW output columns,
+//     run of rows, image). Input rows of the strip + horizontal halo stream into a shared-memory
+//     ring as 2-D TMA boxes of B rows (cp.async.bulk.tensor, completion on a per-slot mbarrier),
+//     issued PF blocks ahead by warp 0, across item boundaries, so the first rows of the next item
+//     arrive while the current one finishes.
+//   * Each chunk of CH (<= 32) rows is processed in two phases by ALL 256 threads:
+//       vertical  - one thread per 2-pixel column word: direct window (w <= 7) or the van Herk /
+//                   Gil-Werman block algorithm with a compile-time register block B and the gap
+//                   minimum tree-reduced from r tail rows and q-1 carried block minima; pixels in
+//                   16-bit lanes so every min/max is one VIMNMX(3).U16x2; results transposed in
+//                   registers (PRMT) into the shared transposed tile;
+//       horizontal- one warp per 4-row (u8) / 2x2-row (u16) group, each lane owning 8 columns:
+//                   direct window or lane-chunk van Herk (prefix written back in place, suffix in
+//                   registers, chunk minima combined for the gap); outputs transposed back to rows
+//                   in registers into a double-buffered output tile;
+//     with one __syncthreads between the phases and one after; multiple CTAs per SM overlap each
+//     other's phases.
+//   * Full chunks leave through one TMA tensor store; ragged chunks with 16-byte stores.
+//   Every pixel is read from HBM once and written once; halo rows/columns are L2 hits.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "morph_phase.cuh"
+
+namespace rmgpu {
+namespace phase {
+cudaError_t dispatch_u8_min(const MorphJob&, int, int, int, int, int, int);
+cudaError_t dispatch_u8_max(const MorphJob&, int, int, int, int, int, int);
+cudaError_t dispatch_u16_min(const MorphJob&, int, int, int, int, int, int);
+cudaError_t dispatch_u16_max(const MorphJob&, int, int, int, int, int, int);
+
+namespace {
+
+struct Choice {
+    int vb, hb, B, q, rh, smem, pf;
+};
+
+bool choose(const MorphJob& j, Choice* c) {
+    if (j.mode != MODE_MIN && j.mode != MODE_MAX) return false;
+    if (j.elem != 1 && j.elem != 2) return false;
+    if ((reinterpret_cast<uintptr_t>(j.src) | j.sp | (j.batch > 1 ? j.simg : 0)) & 15) return false;
+    const int tw = j.elem == 1 ? SG<uint8_t>::TW : SG<uint16_t>::TW;
+    const int w1 = 2 * j.gy;
+    if (j.gy <= 3) {
+        c->vb = 2 * j.gy + 1;
+        c->B = VCH;
+        c->q = 0;
+    } else {
+        double best = 1e30;
+        c->vb = 0;
+        for (int B : {8, 16, 24, 32}) {
+            if (B > w1) continue;
+            const int q = w1 / B, r = w1 - q * B;
+            if (q > QMAX) continue;
+            // min/max per output ~ 3 + (r + q)/B; small blocks pay more per-block overhead
+            const double cost = 3.0 + double(r + q) / B + 4.0 / B;
+            if (cost < best - 1e-9) {
+                best = cost;
+                c->vb = B;
+                c->B = B;
+                c->q = q;
+            }
+        }
+        if (!c->vb) return false;
+    }
+    c->hb = j.gx <= 3 ? 2 * j.gx + 1 : (j.gx <= stream_gxmax(j.elem, 8) ? 8 : 9);
+    if (j.gx > stream_gxmax(j.elem, c->hb)) return false;
+    const int rp = j.elem == 1 ? stream_ring_row<uint8_t>(c->hb) : stream_ring_row<uint16_t>(c->hb);
+    const int blk = c->B * rp;
+    auto smem_of = [&](int pf) {
+        return j.elem == 1 ? phase_smem<uint8_t>(c->hb, c->B, c->q, pf) : phase_smem<uint16_t>(c->hb, c->B, c->q, pf);
+    };
+    // TMA prefetch depth: ~64 KB of input in flight per SM (Little's law at ~1 us loaded DRAM
+    // latency, 6.5 TB/s over 148 SMs), within the shared-memory budget
+    int pf = 1, total = smem_of(pf);
+    if (total > 220 * 1024) return false;
+    if (const char* e = getenv("RMGPU_STREAM_PF")) {
+        pf = std::max(1, atoi(e));
+        total = smem_of(pf);
+    } else {
+        for (int cand = 1; cand <= 16; ++cand) {
+            const int t = smem_of(cand);
+            if (t > 220 * 1024) break;
+            const int occ = std::max(1, std::min(8, (228 * 1024) / (t + 1024)));
+            pf = cand;
+            total = t;
+            if ((long)cand * blk * occ >= 64 * 1024) break;
+        }
+    }
+    c->pf = pf;
+    c->smem = total;
+    // rows per item: ~4 items per resident CTA for balance, >= 4 warm-up lengths
+    const int occ = std::max(1, std::min(8, (228 * 1024) / (total + 1024)));
+    const long strips = (long)((j.W + tw - 1) / tw) * j.batch;
+    const long target = 148L * occ * 4;
+    const long splits = std::max(1L, (target + strips - 1) / strips);
+    int rh = (int)((j.H + splits - 1) / splits);
+    rh = std::max(rh, std::min(j.H, std::max(64, 4 * w1)));
+    rh = (rh + 3) / 4 * 4;
+    if (const char* e = getenv("RMGPU_STREAM_RH")) {
+        const int v = atoi(e);
+        if (v > 0) rh = (v + 3) / 4 * 4;
+    }
+    c->rh = rh;
+    return true;
+}
+
+}  // namespace
+
+bool launch(const MorphJob& j, cudaError_t* err) {
+    Choice c;
+    if (!choose(j, &c)) return false;
+    if (j.elem == 1)
+        *err = j.mode == MODE_MIN ? dispatch_u8_min(j, c.vb, c.hb, c.rh, c.B, c.q, c.pf)
+                                  : dispatch_u8_max(j, c.vb, c.hb, c.rh, c.B, c.q, c.pf);
+    else
+        *err = j.mode == MODE_MIN ? dispatch_u16_min(j, c.vb, c.hb, c.rh, c.B, c.q, c.pf)
+                                  : dispatch_u16_max(j, c.vb, c.hb, c.rh, c.B, c.q, c.pf);
+    return true;
+}
+
+const char* plan_name(const MorphJob& j) {
+    static thread_local char buf[96];
+    MorphJob k = j;
+    k.src = nullptr;
+    k.sp = (size_t)((j.W * j.elem + 15) / 16 * 16);
+    Choice c;
+    if (!choose(k, &c)) return nullptr;
+    snprintf(buf, sizeof(buf), "phase_%s_v%s%d_h%s%d_rh%d_pf%d_smem%dK", j.elem == 1 ? "u8" : "u16",
+             c.vb <= 7 ? "d" : "b", c.vb, c.hb <= 7 ? "d" : "b", c.hb, c.rh, c.pf, c.smem / 1024);
+    return buf;
+}
+
+}  // namespace phase
+}  // namespace rmgpu
