@@ -112,7 +112,8 @@ int check_op_border(int op, int border, unsigned bval, int elem) {
 // One erode / dilate / gradient over the job's rows. Window-1 axes are a copy
 // (separable.cpp:66,88); a 1x1 gradient is all zeros.
 int run_single(MorphJob j) {
-    if (j.gx == 0 && j.gy == 0) {
+    static const bool force_kernel = getenv("RMGPU_FORCE_KERNEL") != nullptr;  // tuning: 1x1 through the kernel
+    if (j.gx == 0 && j.gy == 0 && !force_kernel) {
         for (int b = 0; b < j.batch; ++b) {
             char* d = static_cast<char*>(j.dst) + (size_t)b * j.dimg;
             const char* s = static_cast<const char*>(j.src) + (size_t)b * j.simg;

@@ -53,12 +53,13 @@ bool choose(const MorphJob& j, Choice* c) {
     } else {
         double best = 1e30;
         c->vb = 0;
-        for (int B : {8, 16, 24, 32}) {
+        for (int B : {8, 12, 16, 20, 24, 28, 32}) {
             if (B > w1) continue;
             const int q = w1 / B, r = w1 - q * B;
             if (q > QMAX) continue;
-            // min/max per output ~ 3 + (r + q)/B; small blocks pay more per-block overhead
-            const double cost = 3.0 + double(r + q) / B + 4.0 / B;
+            // min/max per output ~ 3 + (r + q)/B; small blocks pay per-block overhead, the tail
+            // rows are a serial loop
+            const double cost = 3.0 + double(2 * r + q) / B + 6.0 / B;
             if (cost < best - 1e-9) {
                 best = cost;
                 c->vb = B;

@@ -10,11 +10,14 @@ namespace phase {
 
 using namespace stream;
 
-constexpr int PNT = 256;  // threads per CTA: every thread runs both passes
+constexpr int PNT = 256;  // compute threads per CTA (every one runs both passes) + 1 producer warp
 constexpr int PNW = PNT / 32;
 
+// ring slot size: B rows, rounded to 128 bytes (TMA tensor destinations are 128-byte aligned)
+__host__ __device__ constexpr int slot_bytes(int B, int RP) { return (B * RP + 127) / 128 * 128; }
+
 // rows per chunk for block size B (a multiple of B, at most 32)
-__host__ __device__ constexpr int chunk_rows(int B) { return B == 24 ? 24 : 32; }
+__host__ __device__ constexpr int chunk_rows(int B) { return (32 / B) * B; }
 
 struct PPlan {
     int NSB, off_ring, off_vt, off_msc, off_out, total;
@@ -29,9 +32,9 @@ __host__ __device__ inline PPlan make_pplan(int B, int q, int PF) {
     PPlan p;
     // a refilled slot must be older than the previous chunk (warps drift within a chunk)
     p.NSB = q + 1 + PF + CH / B;
-    int o = 64 * 8;
+    int o = 1024;  // mbarriers (<= 64) + store descriptors
     p.off_ring = o;
-    o += p.NSB * B * H::RP;
+    o += p.NSB * slot_bytes(B, H::RP);
     p.off_vt = o;
     o += NGC * H::VTG * G::ESZ;
     p.off_msc = o;
@@ -43,8 +46,35 @@ __host__ __device__ inline PPlan make_pplan(int B, int q, int PF) {
     return p;
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(saddr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(bar)) : "memory");
+}
+
+constexpr int BAR_C = 1;  // named barrier of the compute warps
+
+// Emitting chunks of one item (chunks whose blocks reach the first emitting iteration Lf).
+__device__ __forceinline__ int emitting_chunks(const Item& it, int KB) {
+    int n = 0;
+    for (int c0 = 0; c0 <= it.Lend; c0 += KB)
+        if (min(c0 + KB - 1, it.Lend) >= it.Lf) ++n;
+    return n;
+}
+
 template <typename T, int MODE, int VB, int HB>
-__global__ void __launch_bounds__(PNT)
+__global__ void __launch_bounds__(PNT + 32)
 morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tmap,
                    const __grid_constant__ CUtensorMap omap) {
     using G = SG<T>;
@@ -59,6 +89,7 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
     constexpr int OUTP = TW * sz;
     constexpr int RP = H::RP, NCHP = H::NCHP, VTG = H::VTG, LPG = H::LPG;
     constexpr int SUBG = 32 / LPG;
+    constexpr int SLOT = slot_bytes(B, RP);
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int w1 = 2 * p.gy, w1x = 2 * p.gx;
@@ -73,7 +104,11 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
     const int nitems = nstrips * nrowb * p.batch;
     const int G0 = (int)gridDim.x;
 
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // NSB
+    uint64_t* empty = full + NSB;                          // NSB
+    uint64_t* ofull = empty + NSB;                         // 2
+    uint64_t* oempty = ofull + 2;                          // 2
+    int4* sdesc = reinterpret_cast<int4*>(smem + 512);     // 2 store descriptors {x, y, z, full}
     unsigned char* ring = smem + pl.off_ring;
     unsigned char* vt = smem + pl.off_vt;
     unsigned char* msc0 = smem + pl.off_msc;
@@ -82,69 +117,126 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int k = 0; k < NSB; ++k) mbar_init(&full[k], 1);
+        for (int k = 0; k < NSB; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], 1);
+        }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&ofull[k], 1);
+            mbar_init(&oempty[k], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
     auto item_at = [&](int n) { return (int)blockIdx.x + n * G0; };
 
-    // ---- producer (warp 0): TMA block stream running PF blocks ahead, across items ----------
-    int pn = 0, pk = -1, pslot = 0;
-    bool pvalid = item_at(0) < nitems;
-    Item pit;
-    if (warp == 0 && pvalid) pit = make_item<T>(p, item_at(0), nstrips, nrowb, B, w1, s);
-    auto issue_next = [&]() {
-        if (!pvalid) return;
-        const int slot = pslot;
-        unsigned char* base = ring + (size_t)slot * B * RP;
-        const int yb = pit.y_first + s + pk * B;
-        if (p.use_tma && yb >= p.row_lo && yb + B <= p.row_hi) {
-            if (lane == 0) {
-                mbar_arrive_tx(&full[slot], (uint32_t)(B * RP));
-                tma_box(base, &tmap, pit.xs_b / 4, yb - p.row_lo, pit.b, &full[slot]);
-            }
-        } else {
-            const uint8_t* src = p.src + (size_t)pit.b * p.simg;
-            const int y = yb + lane;
-            const bool inrow = lane < B;
-            const bool outside = p.cmode && (y < p.row_lo || y >= p.row_hi);
-            const unsigned cp = __ballot_sync(0xffffffffu, inrow && !outside);
-            unsigned fillm = __ballot_sync(0xffffffffu, inrow && outside);
-            while (fillm) {
-                const int m = __ffs(fillm) - 1;
-                fillm &= fillm - 1;
-                const uint32_t bw = sz == 1 ? bv * 0x01010101u : bv * 0x00010001u;
-                uint4* row = reinterpret_cast<uint4*>(base + (size_t)m * RP);
-                for (int c = lane; c < RP / 16; c += 32) row[c] = make_uint4(bw, bw, bw, bw);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_tx(&full[slot], (uint32_t)(__popc(cp) * pit.copy_len));
-            __syncwarp();
-            if (inrow && !outside) {
-                const int yc = min(max(y, p.row_lo), p.row_hi - 1);
-                bulk_g2s(base + (size_t)lane * RP + (pit.cb0 - pit.xs_b),
-                         src + (ptrdiff_t)yc * (ptrdiff_t)p.sp + pit.cb0, (uint32_t)pit.copy_len, &full[slot]);
-            }
-        }
-        pslot = pslot + 1 == NSB ? 0 : pslot + 1;
-        if (++pk > pit.Lend) {
-            ++pn;
-            pk = -1;
-            pvalid = item_at(pn) < nitems;
-            if (pvalid) pit = make_item<T>(p, item_at(pn), nstrips, nrowb, B, w1, s);
-        }
-    };
-    if (warp == 0) {
+    if (warp == PNT / 32) {
+        // ======================= producer warp: TMA loads into the ring, TMA stores out ==========
         if (lane == 0 && p.use_tma) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
-        for (int k = 0; k <= PF; ++k) issue_next();
+        int pn = 0, pk = -1, pslot = 0, puse = 0;  // next block: item pn, block pk, slot, slot-use
+        bool pvalid = item_at(0) < nitems;
+        Item pit;
+        if (pvalid) pit = make_item<T>(p, item_at(0), nstrips, nrowb, B, w1, s);
+        // stores to handle: emitting chunks of all this CTA's items
+        int stores_left = 0;
+        for (int n = 0; item_at(n) < nitems; ++n)
+            stores_left += emitting_chunks(make_item<T>(p, item_at(n), nstrips, nrowb, B, w1, s), KB);
+        int sc = 0, pending = -1;
+        while (pvalid || stores_left > 0) {
+            bool did = false;
+            if (pvalid) {
+                int ready = 1;
+                if (lane == 0 && puse > 0) ready = mbar_test(&empty[pslot], (uint32_t)((puse - 1) & 1));
+                ready = __shfl_sync(0xffffffffu, ready, 0);
+                if (ready) {
+                    did = true;
+                    const int slot = pslot;
+                    unsigned char* base = ring + (size_t)slot * SLOT;
+                    const int yb = pit.y_first + s + pk * B;
+                    if (p.use_tma && yb >= p.row_lo && yb + B <= p.row_hi) {
+                        if (lane == 0) {
+                            mbar_arrive_tx(&full[slot], (uint32_t)(B * RP));
+                            tma_box(base, &tmap, pit.xs_b / 4, yb - p.row_lo, pit.b, &full[slot]);
+                        }
+                    } else {
+                        const uint8_t* src = p.src + (size_t)pit.b * p.simg;
+                        const int y = yb + lane;
+                        const bool inrow = lane < B;
+                        const bool outside = p.cmode && (y < p.row_lo || y >= p.row_hi);
+                        const unsigned cp = __ballot_sync(0xffffffffu, inrow && !outside);
+                        unsigned fillm = __ballot_sync(0xffffffffu, inrow && outside);
+                        while (fillm) {
+                            const int m = __ffs(fillm) - 1;
+                            fillm &= fillm - 1;
+                            const uint32_t bw = sz == 1 ? bv * 0x01010101u : bv * 0x00010001u;
+                            uint4* row = reinterpret_cast<uint4*>(base + (size_t)m * RP);
+                            for (int c = lane; c < RP / 16; c += 32) row[c] = make_uint4(bw, bw, bw, bw);
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_tx(&full[slot], (uint32_t)(__popc(cp) * pit.copy_len));
+                        __syncwarp();
+                        if (inrow && !outside) {
+                            const int yc = min(max(y, p.row_lo), p.row_hi - 1);
+                            bulk_g2s(base + (size_t)lane * RP + (pit.cb0 - pit.xs_b),
+                                     src + (ptrdiff_t)yc * (ptrdiff_t)p.sp + pit.cb0, (uint32_t)pit.copy_len,
+                                     &full[slot]);
+                        }
+                    }
+                    if (++pslot == NSB) {
+                        pslot = 0;
+                        ++puse;
+                    }
+                    if (++pk > pit.Lend) {
+                        ++pn;
+                        pk = -1;
+                        pvalid = item_at(pn) < nitems;
+                        if (pvalid) pit = make_item<T>(p, item_at(pn), nstrips, nrowb, B, w1, s);
+                    }
+                }
+            }
+            if (stores_left > 0) {
+                const int ob = sc & 1;
+                int ready = 0;
+                if (lane == 0) ready = mbar_test(&ofull[ob], (uint32_t)((sc >> 1) & 1));
+                ready = __shfl_sync(0xffffffffu, ready, 0);
+                if (ready) {
+                    did = true;
+                    if (lane == 0) {
+                        // the previous store has had a whole chunk to read its buffer: release it
+                        if (pending >= 0) {
+                            bulk_wait_read0();
+                            mbar_arrive(&oempty[pending]);
+                            pending = -1;
+                        }
+                        const int4 d = sdesc[ob];
+                        if (d.w) {
+                            tma_store_box(&omap, d.x, d.y, d.z, outbase + (size_t)ob * CH * OUTP);
+                            bulk_commit();
+                            pending = ob;
+                        } else {
+                            mbar_arrive(&oempty[ob]);  // copied by the compute warps already
+                        }
+                    }
+                    ++sc;
+                    --stores_left;
+                }
+            }
+            if (!did) __nanosleep(40);
+        }
+        if (lane == 0) {
+            if (pending >= 0) mbar_arrive(&oempty[pending]);
+            bulk_wait_all();
+        }
+        return;
     }
 
+    // =========================== compute warps (PNT threads) ===================================
     auto op2 = [](uint32_t x, uint32_t y) { return red2_u16x2<MODE>(x, y); };
     auto op3 = [](uint32_t x, uint32_t y, uint32_t z) { return red3_u16x2<MODE>(x, y, z); };
     constexpr uint32_t IDV = MODE == MODE_MIN ? 0xFFFFFFFFu : 0u;
 
-    // consumed block stream (all threads): slot/parity of current block and of blocks -1, -q, -q-1
+    // consumed block stream: slot/parity of current block and of blocks -1, -q, -q-1
     int seq = 0, sL = 0, ph = 0;
     int sL1 = NSB - 1, sQ = ((-q) % NSB + NSB) % NSB, sQ1 = ((-q - 1) % NSB + NSB) % NSB;
     auto advance = [&]() {
@@ -155,17 +247,23 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
         sQ1 = sQ;
         sQ = sQ + 1 == NSB ? 0 : sQ + 1;
     };
-    int chunk = 0;  // output-buffer parity counter
+    int rel = 0, rslot = 0;  // blocks released to the producer: seq < rel
+    auto release_below = [&](int upto) {
+        if (tid == 0)
+            while (rel < upto) {
+                mbar_arrive(&empty[rslot]);
+                rslot = rslot + 1 == NSB ? 0 : rslot + 1;
+                ++rel;
+            }
+    };
+    int chunk = 0;  // emitting chunks so far (output buffer parity / use count)
 
-    // horizontal identity: warp -> row groups (SUBG per pass), lane -> 8-column chunk
     const int sub = lane / LPG, lam = lane % LPG;
     const int q8 = w1x >> 3, r8 = w1x & 7;
 
     for (int n = 0; item_at(n) < nitems; ++n) {
         const Item it = make_item<T>(p, item_at(n), nstrips, nrowb, B, w1, s);
         uint8_t* dst = p.dst + (size_t)it.b * p.dimg;
-        // vertical identity: thread -> 2-pixel column word (threads past the strip mirror the last
-        // word and write a scratch column, so the sweep has no divergent branches)
         const bool real = tid < it.nwv;
         const int t = real ? tid : it.nwv - 1;
         int load_off = 0;
@@ -192,10 +290,9 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
             }
         };
         const unsigned char* rbase = ring + load_off;
-        auto sbase = [&](int slot) { return rbase + (size_t)slot * (B * RP); };
+        auto sbase = [&](int slot) { return rbase + (size_t)slot * SLOT; };
 
         // block -1 of this item
-        if (warp == 0 && seq > 0) issue_next();
         mbar_wait(&full[sL], (uint32_t)ph);
         advance();
 
@@ -205,13 +302,16 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
 
         for (int c0 = 0; c0 <= it.Lend; c0 += KB) {
             // ================= vertical phase: KB blocks of B rows into the transposed tile =========
+            const int tci = chunk < 60 ? chunk : 59;
+            if (warp == 0) RM_TRACE(tci * 8 + 0);
             bool emit_any = false;
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
                 const int L = c0 + kb;
                 if (L > it.Lend) break;
-                if (warp == 0) issue_next();
+                if (warp == 0 && kb == 0) RM_TRACE(tci * 8 + 1);
                 mbar_wait(&full[sL], (uint32_t)ph);
+                if (warp == 0 && kb == 0) RM_TRACE(tci * 8 + 2);
                 const bool emit = L >= it.Lf;
                 emit_any |= emit;
                 const unsigned char* lead = sbase(sL);
@@ -254,22 +354,17 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
 #pragma unroll
                     for (int m = 1; m < B; ++m) P[m] = op2(P[m - 1], ldw(lead + m * RP));
                     if (emit) {
+                        // gap = tail r rows of block L-q + whole blocks L-q+1 .. L-1 (r is small:
+                        // the planner picks B to minimise it)
                         const unsigned char* tb = sbase(sQ);
                         const unsigned char* tt = tb + (B - r) * RP;
-                        uint32_t v[B + QMAX];
-#pragma unroll
-                        for (int i = 0; i < B - 1; ++i) v[i] = i < r ? ldw(tt + i * RP) : IDV;
-#pragma unroll
-                        for (int k = 0; k < QMAX - 1; ++k) v[B - 1 + k] = k < q - 1 ? M[k] : IDV;
-                        constexpr int NV = B - 1 + QMAX - 1;
-#pragma unroll
-                        for (int i = 0; i < NV; i += 3)
-                            v[i / 3] = op3(v[i], i + 1 < NV ? v[i + 1] : IDV, i + 2 < NV ? v[i + 2] : IDV);
-                        constexpr int NV2 = (NV + 2) / 3;
                         uint32_t gap = IDV;
+                        for (int i = 0; i < r; ++i) gap = op2(gap, ldw(tt + i * RP));
 #pragma unroll
-                        for (int i = 0; i < NV2; i += 3)
-                            gap = op3(gap, v[i], op2(i + 1 < NV2 ? v[i + 1] : IDV, i + 2 < NV2 ? v[i + 2] : IDV));
+                        for (int k = 0; k + 1 < QMAX; k += 2) {
+                            const uint32_t a = k < q - 1 ? M[k] : IDV, b = k + 1 < q - 1 ? M[k + 1] : IDV;
+                            gap = op3(gap, a, b);
+                        }
                         const unsigned char* ta = sbase(sQ1) + (B - r) * RP;
                         const unsigned char* tbb = tb - r * RP;
                         uint32_t acc = gap;
@@ -287,14 +382,15 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
                 advance();
             }
             if (!emit_any) continue;  // warm-up chunk: nothing to hand over (uniform across the CTA)
-            // the previous chunk's TMA store must be done reading its output buffer
-            if (tid == 0 && p.use_tma_out) bulk_wait_read0();
-            __syncthreads();  // transposed tile complete
+            if (warp == 0) RM_TRACE(tci * 8 + 3);
+            bar_sync(BAR_C, PNT);  // transposed tile complete
+            if (warp == 0) RM_TRACE(tci * 8 + 4);
 
             // ================= horizontal phase: one warp per row group ===============================
             const int oC = s + c0 * B - w1;  // output row of chunk row 0 (relative to the item)
             const int ob = chunk & 1;
             unsigned char* outt = outbase + (size_t)ob * CH * OUTP;
+            if (chunk >= 2) mbar_wait(&oempty[ob], (uint32_t)(((chunk >> 1) - 1) & 1));
             for (int g0 = warp * SUBG; g0 < NGC; g0 += PNW * SUBG) {
                 const int g = g0 + sub;
                 const unsigned char* rowg = vt + (size_t)g * VTG * ESZ;
@@ -376,16 +472,8 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
                     }
                     __syncwarp();
                     const int k = lam;
-                    constexpr int QM8 = H::GXMAX / 4 + 1;
-                    LW<T> mv[QM8 + 2];
-#pragma unroll
-                    for (int i = 0; i < QM8 + 2; ++i) mv[i] = lid<T, MODE>();
-#pragma unroll
-                    for (int i = 1; i < QM8; ++i)
-                        if (i < q8) mv[i - 1] = ld8(msc + (k + i) * ESZ);
                     LW<T> Fa = lid<T, MODE>();
-#pragma unroll
-                    for (int i = 0; i < QM8; i += 3) Fa = lop<MODE>(Fa, lop3<MODE>(mv[i], mv[i + 1], mv[i + 2]));
+                    for (int i = 1; i < q8; ++i) Fa = lop<MODE>(Fa, ld8(msc + (k + i) * ESZ));
                     const LW<T> Fb = lop<MODE>(Fa, ld8(msc + (k + q8) * ESZ));
                     const unsigned char* pa = scr + (r8 * NCHP + k + q8) * ESZ;
                     const unsigned char* pbb = scr + ((r8 - 8) * NCHP + k + q8 + 1) * ESZ;
@@ -400,14 +488,13 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
             }
             const int rlo = max(0, -oC), rhi = min(CH, it.rh - oC);
             const bool full_chunk = p.use_tma_out && rlo == 0 && rhi == CH && it.x0 + TW <= p.W;
-            if (full_chunk) fence_async_smem();
-            __syncthreads();  // output tile complete, transposed tile free
-            if (full_chunk) {
-                if (tid == 0) {
-                    tma_store_box(&omap, it.x0 * sz, it.y0 + oC, it.b, outt);
-                    bulk_commit();
-                }
-            } else {
+            if (warp == 0) RM_TRACE(tci * 8 + 5);
+            if (full_chunk) fence_async_smem();  // emits visible to the TMA store (async proxy)
+            bar_sync(BAR_C, PNT);                // output tile complete, transposed tile free
+            if (warp == 0) RM_TRACE(tci * 8 + 6);
+            const int g_last = seq - 1;          // last block consumed by this chunk
+            const bool item_done = c0 + KB > it.Lend;
+            if (!full_chunk) {
                 const int cols = min(TW, p.W - it.x0);
                 const int row_bytes = cols * sz;
                 const bool vec = (((uintptr_t)dst | p.dp) & 15) == 0 && cols == TW;
@@ -424,11 +511,18 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
                         dst[(size_t)(it.y0 + oC + rr) * p.dp + (size_t)it.x0 * sz + b] = outt[(size_t)rr * OUTP + b];
                     }
                 }
+                bar_sync(BAR_C, PNT);  // copy finished: the producer may hand the buffer back
             }
+            if (tid == 0) {
+                sdesc[ob] = make_int4(it.x0 * sz, it.y0 + oC, it.b, full_chunk ? 1 : 0);
+                mbar_arrive(&ofull[ob]);
+            }
+            // blocks no iteration after this chunk reads: everything below seq (g_last - q) of this
+            // item, or the whole item when it is finished
+            release_below(item_done ? g_last + 1 : g_last - q);
             ++chunk;
         }
     }
-    if (tid == 0 && p.use_tma_out) bulk_wait_all();
 }
 
 template <typename T, int MODE, int VB, int HB>
@@ -452,6 +546,8 @@ cudaError_t launch_phase_variant(const MorphJob& j, int rh, int B, int q, int pf
     p.rh = rh;
     p.pf = pf;
     p.batch = j.batch;
+    p.trace = g_trace;
+    p.trace_cta = g_trace_cta;
     CUtensorMap map, omap;
     p.use_tma = encode_input_map(j, HG<T, HB>::RP / 4, B, &map) ? 1 : 0;
     p.use_tma_out = encode_output_map(j, G::TW * (int)sizeof(T), chunk_rows(B), &omap) ? 1 : 0;
@@ -461,18 +557,18 @@ cudaError_t launch_phase_variant(const MorphJob& j, int rh, int B, int q, int pf
     if (e != cudaSuccess) return e;
     const long items = (long)cdiv(j.W, G::TW) * cdiv(j.H, rh) * j.batch;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PNT, pl.total);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PNT + 32, pl.total);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long ctas = std::max(1L, std::min(items, (long)sms * std::max(1, occ)));
-    kern<<<dim3((unsigned)ctas), PNT, pl.total, j.stream>>>(p, map, omap);
+    kern<<<dim3((unsigned)ctas), PNT + 32, pl.total, j.stream>>>(p, map, omap);
     count_launch();
     return cudaGetLastError();
 }
 
-#define RM_PHASE_V(X) X(1) X(3) X(5) X(7) X(8) X(16) X(24) X(32)
+#define RM_PHASE_V(X) X(1) X(3) X(5) X(7) X(8) X(12) X(16) X(20) X(24) X(28) X(32)
 #define RM_PHASE_H(X) X(1) X(3) X(5) X(7) X(8) X(9)
 
 template <typename T, int MODE, int VB>

@@ -15,7 +15,7 @@ namespace stream {
 // horizontal warps: one per 4-row group of a chunk of B rows (2..8)
 __host__ __device__ constexpr int nhw_of(int B) { return B / 4 < 2 ? 2 : (B / 4 > 8 ? 8 : B / 4); }
 constexpr int QMAX = 6;                // whole blocks between suffix run and prefix block (registers)
-constexpr int VCH = 32;                // rows per iteration for the direct vertical variants
+constexpr int VCH = 16;                // rows per iteration for the direct vertical variants
 constexpr int HC = 8;                  // horizontal lane chunk (block variant)
 
 // named barrier ids (0 is __syncthreads)
