@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "../../include/rmgpu.h"
 #include "common.cuh"
@@ -21,6 +22,67 @@
 namespace rmgpu {
 std::atomic<unsigned long long> g_launch_count{0};
 }
+
+
+namespace rmgpu {
+namespace {
+struct OccKey {
+    const void* kern;
+    int dev, threads, smem;
+    bool operator==(const OccKey& o) const {
+        return kern == o.kern && dev == o.dev && threads == o.threads && smem == o.smem;
+    }
+};
+struct OccHash {
+    size_t operator()(const OccKey& k) const {
+        return std::hash<const void*>()(k.kern) ^ ((size_t)k.dev << 48) ^ ((size_t)k.threads << 32) ^ (size_t)k.smem;
+    }
+};
+std::mutex g_occ_mu;
+std::unordered_map<OccKey, int, OccHash> g_occ;
+std::unordered_map<OccKey, int, OccHash> g_smem_set;  // (kern, dev) -> dynamic smem limit set so far
+int g_sms[64];
+}  // namespace
+
+int kernel_occupancy(const void* kern, int threads, int smem, cudaError_t* err) {
+    int dev = 0;
+    *err = cudaGetDevice(&dev);
+    if (*err != cudaSuccess) return 0;
+    const OccKey key{kern, dev, threads, smem};
+    {
+        std::lock_guard<std::mutex> g(g_occ_mu);
+        auto it = g_occ.find(key);
+        if (it != g_occ.end()) return it->second;
+    }
+    {
+        // the limit only ever grows: a smaller later setting would break cached larger launches
+        std::lock_guard<std::mutex> g(g_occ_mu);
+        int& cur = g_smem_set[OccKey{kern, dev, 0, 0}];
+        if (smem > cur) {
+            *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (*err != cudaSuccess) return 0;
+            cur = smem;
+        }
+    }
+    int occ = 0;
+    *err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+    if (*err != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> g(g_occ_mu);
+    g_occ[key] = occ;
+    return occ;
+}
+
+int device_sm_count() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (dev < 0 || dev >= 64) return 148;
+    int v = __atomic_load_n(&g_sms[dev], __ATOMIC_RELAXED);
+    if (v) return v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    __atomic_store_n(&g_sms[dev], v, __ATOMIC_RELAXED);
+    return v;
+}
+}  // namespace rmgpu
 
 using rmgpu::MorphJob;
 
@@ -123,6 +185,10 @@ int run_single(MorphJob j) {
         return RMGPU_OK;
     }
     cudaError_t e = cudaSuccess;
+    if (!g_disable_stream && !g_prefer_stream && rmgpu::col::launch(j, &e)) {
+        if (e != cudaSuccess) return cuda_fail(e, "register-streaming morph kernel");
+        return RMGPU_OK;
+    }
     if (!g_disable_stream && !g_prefer_stream && rmgpu::phase::launch(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "phase morph kernel");
         return RMGPU_OK;
@@ -355,6 +421,8 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
     j.mode = op == RMGPU_ERODE ? rmgpu::MODE_MIN : op == RMGPU_DILATE ? rmgpu::MODE_MAX : rmgpu::MODE_GRAD;
     if (op == RMGPU_OPEN || op == RMGPU_CLOSE) j.mode = rmgpu::MODE_MIN;
     if (j.gx == 0 && j.gy == 0) return "copy";
+    if (!g_disable_stream && !g_prefer_stream)
+        if (const char* n = rmgpu::col::plan_name(j)) return n;
     if (!g_disable_stream && !g_prefer_stream)
         if (const char* n = rmgpu::phase::plan_name(j)) return n;
     if (!g_disable_stream)

@@ -26,6 +26,12 @@ struct MorphJob {
     cudaStream_t stream = nullptr;
 };
 
+// ---- launch bookkeeping (capi.cu): cached per (kernel, device) so a launch costs no extra
+// driver round trips. Sets the dynamic shared-memory limit on first use; returns resident CTAs
+// per SM (0 and an error on failure).
+int kernel_occupancy(const void* kern, int threads, int smem, cudaError_t* err);
+int device_sm_count();
+
 // ---- generic paths (morph_generic.cu): any window, any pitch --------------------------------
 bool generic_tile_fits(const MorphJob& j);
 cudaError_t launch_generic_tile(const MorphJob& j);
@@ -53,6 +59,12 @@ namespace phase {
 bool launch(const MorphJob& j, cudaError_t* err);
 const char* plan_name(const MorphJob& j);
 }  // namespace phase
+
+// ---- register-streaming fused path for small windows (morph_col.cu), preferred over phase ----
+namespace col {
+bool launch(const MorphJob& j, cudaError_t* err);
+const char* plan_name(const MorphJob& j);
+}  // namespace col
 
 // ---- transposes (transpose.cu) ---------------------------------------------------------------
 cudaError_t launch_transpose(const void* src, size_t sp, void* dst, size_t dp, int W, int H,

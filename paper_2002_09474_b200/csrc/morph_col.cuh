@@ -1,0 +1,455 @@
+// morph_col.cuh -- K1 v4: register-streaming fused separable erosion / dilation for small
+// windows (both wings <= 3, i.e. w <= 7), u8 and u16. Design notes in morph_col.cu.
+#pragma once
+
+#include <algorithm>
+#include <type_traits>
+
+#include "morph_stream.cuh"  // PTX helpers (mbarrier, TMA), tensor-map encoders, red*_u16x2
+
+namespace rmgpu {
+namespace col {
+
+using stream::bulk_g2s;
+using stream::fence_async_smem;
+using stream::mbar_arrive_tx;
+using stream::mbar_init;
+using stream::mbar_wait;
+using stream::tma_box;
+
+constexpr int WPB = 4;               // warps per CTA (independent pipelines sharing one smem block)
+constexpr int BR = 8;                // rows per TMA block
+constexpr int NS = 3;                // ring slots per warp
+constexpr int HALO = 16;             // halo bytes left / right of a strip row
+constexpr int SB = 512;              // strip bytes per row (32 lanes x 16 B)
+constexpr int RB = SB + 2 * HALO;    // bytes per staged row (544)
+constexpr int SLOTB = BR * RB;       // 4352 = 34 x 128 (TMA destinations stay 128-B aligned)
+constexpr int WARPB = NS * SLOTB;
+constexpr int HDR = 128;             // mbarriers
+constexpr int SMEM = HDR + WPB * WARPB;
+constexpr int GMAX = 3;
+
+struct ColParams {
+    const uint8_t* src;  // output row 0 of image 0
+    size_t sp;
+    uint8_t* dst;
+    size_t dp;
+    int W, H;
+    int row_lo, row_hi;  // valid input rows relative to output row 0
+    int cmode;
+    uint32_t bval;
+    size_t simg, dimg;
+    int batch;
+    int R;               // output rows per item
+    int nstrips, nbands;
+    int use_tma;
+};
+
+// item n -> (image, band, strip); strips fastest so neighbouring warps share halo rows in L2
+struct CItem {
+    int b, y0, x0, rows_out, nblk;
+};
+template <typename T, int GY>
+__device__ __forceinline__ CItem col_item(const ColParams& p, int n) {
+    CItem it;
+    const int per_img = p.nstrips * p.nbands;
+    it.b = n / per_img;
+    const int rem = n - it.b * per_img;
+    const int band = rem / p.nstrips;
+    const int strip = rem - band * p.nstrips;
+    it.y0 = band * p.R;
+    it.x0 = strip * (SB / (int)sizeof(T));
+    it.rows_out = min(p.R, p.H - it.y0);
+    it.nblk = (it.rows_out + 2 * GY + BR - 1) / BR;
+    return it;
+}
+
+template <int MODE>
+__device__ __forceinline__ uint32_t op2(uint32_t a, uint32_t b) {
+    return red2_u16x2<MODE>(a, b);
+}
+template <int MODE>
+__device__ __forceinline__ uint32_t op3(uint32_t a, uint32_t b, uint32_t c) {
+    return red3_u16x2<MODE>(a, b, c);
+}
+// reduction over N consecutive words of a list (N odd, <= 7)
+template <int MODE, int N>
+__device__ __forceinline__ uint32_t opn(const uint32_t* v) {
+    if constexpr (N == 1) return v[0];
+    else if constexpr (N == 3) return op3<MODE>(v[0], v[1], v[2]);
+    else if constexpr (N == 5) return op3<MODE>(op3<MODE>(v[0], v[1], v[2]), v[3], v[4]);
+    else return op3<MODE>(op3<MODE>(op3<MODE>(v[0], v[1], v[2]), v[3], v[4]), v[5], v[6]);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Per-row word sets. u8: a lane owns 16 pixels = 4 raw words; min/max run on 16-bit lanes of
+// the raw word (odd pixels, in the high bytes: the high byte of a 16-bit min/max is the min/max
+// of the high bytes) and of its byte-swapped copy (even pixels) -- one PRMT per 4 pixels, no
+// unpacking. u16: a lane owns 8 pixels = 4 u16x2 words. Both carry 2 extra words: the column
+// word(s) just left of the strip (lane 0) / right of it (lane 31).
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+struct RowW;
+template <>
+struct RowW<uint8_t> {
+    static constexpr int N = 10;  // S0..S3 (even pixels), R0..R3 (odd pixels), XS, XR
+};
+template <>
+struct RowW<uint16_t> {
+    static constexpr int N = 6;   // w0..w3, X0, X1
+};
+
+template <typename T, int MODE, int GX, int GY, bool EDGE>
+struct ColCore {
+    static constexpr int NW = RowW<T>::N;
+    static constexpr int WV = 2 * GY + 1;
+    static constexpr int sz = sizeof(T);
+    static constexpr int PXL = 16 / sz;  // pixels per lane
+
+    // load one staged row into expanded words (+ border columns fixed in EDGE strips)
+    static __device__ __forceinline__ void load_row(const unsigned char* row, int lane, uint32_t* e,
+                                                    const uint32_t* sel, uint32_t fill_l, uint32_t fill_r,
+                                                    const ColParams& p, int x0) {
+        const uint4 m = *reinterpret_cast<const uint4*>(row + HALO + lane * 16);
+        uint32_t w[4] = {m.x, m.y, m.z, m.w};
+        uint32_t x[2];
+        const int xo = lane == 0 ? HALO - 8 : HALO + SB;
+        const uint2 xx = *reinterpret_cast<const uint2*>(row + xo);
+        if constexpr (sz == 1) {
+            x[0] = lane == 0 ? xx.y : xx.x;  // left: bytes x0-4..x0-1; right: x0+512..x0+515
+        } else {
+            x[0] = xx.x;
+            x[1] = xx.y;
+        }
+        if constexpr (EDGE) {
+            uint32_t fl = fill_l, fr = fill_r;
+            if (p.cmode == 0) {
+                // replicate: the first / last image pixel of this row
+                if constexpr (sz == 1) {
+                    fl = row[HALO] * 0x01010101u;
+                    fr = row[HALO + min(p.W - 1 - x0, SB + 3)] * 0x01010101u;
+                } else {
+                    fl = *reinterpret_cast<const uint16_t*>(row + HALO) * 0x00010001u;
+                    fr = *reinterpret_cast<const uint16_t*>(row + HALO + min(p.W - 1 - x0, SB / 2 + 3) * 2) * 0x00010001u;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[k] = prmt(w[k], fr, sel[k]);
+            const uint32_t fx = lane == 0 ? fl : fr;
+            x[0] = prmt(x[0], fx, sel[4]);
+            if constexpr (sz == 2) x[1] = prmt(x[1], fx, sel[5]);
+        }
+        if constexpr (sz == 1) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                e[k] = prmt(w[k], w[k], 0x2301);  // even pixels into the high bytes
+                e[4 + k] = w[k];                  // odd pixels already there
+            }
+            e[8] = prmt(x[0], x[0], 0x2301);
+            e[9] = x[0];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) e[k] = w[k];
+            e[4] = x[0];
+            e[5] = x[1];
+        }
+    }
+
+    // horizontal window over one vertically reduced row; returns the 4 packed output words
+    static __device__ __forceinline__ uint4 horizontal(const uint32_t* v, int lane) {
+        uint32_t o[4];
+        if constexpr (sz == 1) {
+            // S(k) / R(k) for k = -1..4 (k = -1 / 4 from the neighbouring lanes or the extra word)
+            uint32_t S[6], Rr[6];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                S[k + 1] = v[k];
+                Rr[k + 1] = v[4 + k];
+            }
+            S[0] = S[5] = Rr[0] = Rr[5] = 0;
+            if constexpr (GX >= 1) {  // R(-1), S(4)
+                const uint32_t rl = __shfl_up_sync(0xffffffffu, v[7], 1);
+                const uint32_t sr = __shfl_down_sync(0xffffffffu, v[0], 1);
+                Rr[0] = lane == 0 ? v[9] : rl;
+                S[5] = lane == 31 ? v[8] : sr;
+            }
+            if constexpr (GX >= 2) {  // S(-1), R(4)
+                const uint32_t sl = __shfl_up_sync(0xffffffffu, v[3], 1);
+                const uint32_t rr = __shfl_down_sync(0xffffffffu, v[4], 1);
+                S[0] = lane == 0 ? v[8] : sl;
+                Rr[5] = lane == 31 ? v[9] : rr;
+            }
+            // U(i) = {p_i, p_{i+2}} for i = -GX .. 13+GX; U(4k)=S(k), U(4k+1)=R(k),
+            // U(4k+2)=PRMT(S(k),S(k+1)), U(4k+3)=PRMT(R(k),R(k+1))
+            constexpr int UB = GX;  // U index offset
+            uint32_t U[14 + 2 * GX];
+#pragma unroll
+            for (int i = -GX; i < 14 + GX; ++i) {
+                const int k = (i + 4) / 4 - 1, m = (i + 4) % 4;
+                uint32_t u;
+                if (m == 0) u = S[k + 1];
+                else if (m == 1) u = Rr[k + 1];
+                else if (m == 2) u = prmt(S[k + 1], S[k + 2], 0x5432);
+                else u = prmt(Rr[k + 1], Rr[k + 2], 0x5432);
+                U[i + UB] = u;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t oe = opn<MODE, 2 * GX + 1>(&U[4 * k - GX + UB]);
+                const uint32_t oo = opn<MODE, 2 * GX + 1>(&U[4 * k + 1 - GX + UB]);
+                o[k] = prmt(oe, oo, 0x7351);
+            }
+        } else {
+            // Wf(k) for k = -2..5
+            uint32_t Wf[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) Wf[k + 2] = v[k];
+            if constexpr (GX >= 1) {
+                const uint32_t l1 = __shfl_up_sync(0xffffffffu, v[3], 1);
+                const uint32_t r0 = __shfl_down_sync(0xffffffffu, v[0], 1);
+                Wf[1] = lane == 0 ? v[5] : l1;
+                Wf[6] = lane == 31 ? v[4] : r0;
+                if constexpr (GX >= 3) {
+                    const uint32_t l2 = __shfl_up_sync(0xffffffffu, v[2], 1);
+                    const uint32_t r1 = __shfl_down_sync(0xffffffffu, v[1], 1);
+                    Wf[0] = lane == 0 ? v[4] : l2;
+                    Wf[7] = lane == 31 ? v[5] : r1;
+                } else {
+                    Wf[0] = Wf[7] = 0;
+                }
+            } else {
+                Wf[0] = Wf[1] = Wf[6] = Wf[7] = 0;
+            }
+            // U(i) = {p_i, p_{i+1}} for i = -GX .. 6+GX
+            constexpr int UB = GX;
+            uint32_t U[7 + 2 * GX];
+#pragma unroll
+            for (int i = -GX; i < 7 + GX; ++i) {
+                const int k = (i + 4) / 2 - 2, m = (i + 4) % 2;
+                U[i + UB] = m == 0 ? Wf[k + 2] : prmt(Wf[k + 2], Wf[k + 3], 0x5432);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[k] = opn<MODE, 2 * GX + 1>(&U[2 * k - GX + UB]);
+        }
+        return make_uint4(o[0], o[1], o[2], o[3]);
+    }
+};
+
+template <typename T, int MODE, int GX, int GY>
+__global__ void __launch_bounds__(WPB * 32)
+morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int sz = sizeof(T);
+    constexpr int PXL = 16 / sz;
+    constexpr int SWPX = SB / sz;
+    constexpr int WV = 2 * GY + 1;
+    constexpr int NW = RowW<T>::N;
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + wib * NS;
+    unsigned char* ring = smem + HDR + wib * WARPB;
+    if (lane == 0) {
+        for (int k = 0; k < NS; ++k) mbar_init(&bars[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+
+    const int nwarps = gridDim.x * WPB;
+    const int gw = blockIdx.x * WPB + wib;
+    const int nitems = p.nstrips * p.nbands * p.batch;
+    if (gw >= nitems) return;
+    const uint32_t bv = sz == 1 ? (p.bval & 0xFF) * 0x01010101u : (p.bval & 0xFFFF) * 0x00010001u;
+
+    // ---- producer side (all lanes run it; lane 0 / lanes < BR issue) ----------------------------
+    int in_ = gw, ib = 0;  // next block to issue: item index, block within item
+    CItem iit = col_item<T, GY>(p, in_);
+    int iseq = 0;          // blocks issued
+    auto issue = [&]() {
+        if (in_ >= nitems) return;
+        const int slot = iseq % NS;
+        unsigned char* dstb = ring + slot * SLOTB;
+        uint64_t* bar = &bars[slot];
+        const int yb = iit.y0 - GY + ib * BR;
+        const int xb = iit.x0 * sz - HALO;  // byte column of the staged row start
+        if (p.use_tma && yb >= p.row_lo && yb + BR <= p.row_hi) {
+            if (lane == 0) {
+                mbar_arrive_tx(bar, (uint32_t)SLOTB);
+                tma_box(dstb, &tmap, xb / 4, yb - p.row_lo, iit.b, bar);
+            }
+        } else {
+            // border block: one bulk copy per row (clamped row / constant fill), clipped columns
+            const int y = yb + lane;
+            const bool inrow = lane < BR;
+            const bool outside = p.cmode && (y < p.row_lo || y >= p.row_hi);
+            const int c0 = max(xb, 0);
+            const int c1 = min(xb + RB, (int)p.sp);
+            const int len = c1 - c0;
+            const unsigned cp = __ballot_sync(0xffffffffu, inrow && !outside);
+            unsigned fillm = __ballot_sync(0xffffffffu, inrow && outside);
+            while (fillm) {
+                const int r = __ffs(fillm) - 1;
+                fillm &= fillm - 1;
+                for (int c = lane; c < RB / 16; c += 32)
+                    reinterpret_cast<uint4*>(dstb + r * RB)[c] = make_uint4(bv, bv, bv, bv);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_tx(bar, (uint32_t)(__popc(cp) * len));
+            __syncwarp();
+            if (inrow && !outside) {
+                const int yc = min(max(y, p.row_lo), p.row_hi - 1);
+                bulk_g2s(dstb + lane * RB + (c0 - xb),
+                         p.src + (size_t)iit.b * p.simg + (ptrdiff_t)yc * (ptrdiff_t)p.sp + c0, (uint32_t)len, bar);
+            }
+        }
+        ++iseq;
+        if (++ib == iit.nblk) {
+            ib = 0;
+            in_ += nwarps;
+            if (in_ < nitems) iit = col_item<T, GY>(p, in_);
+        }
+    };
+    for (int k = 0; k < NS; ++k) issue();
+
+    // ---- consumer --------------------------------------------------------------------------------
+    int cseq = 0;  // blocks consumed
+    for (int n = gw; n < nitems; n += nwarps) {
+        const CItem it = col_item<T, GY>(p, n);
+        const bool edge = it.x0 == 0 || it.x0 + SWPX + 4 > p.W;
+        uint8_t* dst = p.dst + (size_t)it.b * p.dimg + (size_t)it.x0 * sz + (size_t)lane * 16;
+        auto run = [&](auto edge_tag) {
+            constexpr bool EDGE = decltype(edge_tag)::value;
+            using C = ColCore<T, MODE, GX, GY, EDGE>;
+            // per-lane column selectors for the border strips: keep byte j, or take the fill word
+            uint32_t sel[6] = {0x3210, 0x3210, 0x3210, 0x3210, 0x3210, 0x3210};
+            uint32_t fill_l = bv, fill_r = bv;
+            int store_bytes = 16;
+            if constexpr (EDGE) {
+                auto selw = [&](int px0, int npx) {  // word of npx pixels starting at column px0
+                    uint32_t s = 0;
+                    for (int j = 0; j < 4; ++j) {
+                        const int px = px0 + j / sz;
+                        const bool ok = px >= 0 && px < p.W;
+                        s |= (uint32_t)(ok ? j : 4 + (j % sz)) << (4 * j);
+                    }
+                    (void)npx;
+                    return s;
+                };
+                const int pxl = it.x0 + lane * PXL;
+                for (int k = 0; k < 4; ++k) sel[k] = selw(pxl + k * (4 / sz), 4 / sz);
+                const int xpx = lane == 0 ? it.x0 - 4 : it.x0 + SWPX;
+                sel[4] = selw(xpx, 4 / sz);
+                sel[5] = selw(xpx + 4 / sz, 4 / sz);
+                store_bytes = max(0, min(16, (p.W - pxl) * sz));
+            }
+            uint32_t E[WV][NW];
+            const int rows_in = it.rows_out + 2 * GY;
+            const unsigned char* rowp = nullptr;
+            int rib = BR;  // row index within the current block (BR = need a new block)
+            int o = -2 * GY;  // output row of the newest input row
+            for (int t0 = 0; t0 < rows_in; t0 += WV) {
+#pragma unroll
+                for (int j = 0; j < WV; ++j) {
+                    if (t0 + j < rows_in) {
+                        if (rib == BR) {
+                            const int slot = cseq % NS;
+                            mbar_wait(&bars[slot], (uint32_t)((cseq / NS) & 1));
+                            rowp = ring + slot * SLOTB;
+                            rib = 0;
+                        }
+                        C::load_row(rowp, lane, E[j], sel, fill_l, fill_r, p, it.x0);
+                        rowp += RB;
+                        ++rib;
+                        if (rib == BR || t0 + j == rows_in - 1) {
+                            // block fully read: hand the slot back to the producer
+                            ++cseq;
+                            __syncwarp();
+                            fence_async_smem();
+                            issue();
+                            rib = BR;
+                        }
+                        if (o >= 0) {
+                            uint32_t v[NW];
+#pragma unroll
+                            for (int w = 0; w < NW; ++w) {
+                                uint32_t col[WV];
+#pragma unroll
+                                for (int r = 0; r < WV; ++r) col[r] = E[r][w];
+                                v[w] = opn<MODE, WV>(col);
+                            }
+                            const uint4 out = C::horizontal(v, lane);
+                            uint8_t* d = dst + (size_t)(it.y0 + o) * p.dp;
+                            if (!EDGE || store_bytes == 16) {
+                                *reinterpret_cast<uint4*>(d) = out;
+                            } else if (store_bytes > 0) {
+                                const uint32_t ow[4] = {out.x, out.y, out.z, out.w};
+                                for (int bI = 0; bI < store_bytes; ++bI) d[bI] = (uint8_t)(ow[bI >> 2] >> (8 * (bI & 3)));
+                            }
+                        }
+                        ++o;
+                    }
+                }
+            }
+        };
+        if (edge) run(std::true_type{});
+        else run(std::false_type{});
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+template <typename T, int MODE, int GX, int GY>
+cudaError_t launch_col_variant(const MorphJob& j, int R) {
+    ColParams p{};
+    p.src = static_cast<const uint8_t*>(j.src);
+    p.sp = j.sp;
+    p.dst = static_cast<uint8_t*>(j.dst);
+    p.dp = j.dp;
+    p.W = j.W;
+    p.H = j.H;
+    p.row_lo = -j.above;
+    p.row_hi = j.H + j.below;
+    p.cmode = j.cmode;
+    p.bval = j.bval;
+    p.simg = j.simg;
+    p.dimg = j.dimg;
+    p.batch = j.batch;
+    p.R = R;
+    p.nstrips = cdiv(j.W * (int)sizeof(T), SB);
+    p.nbands = cdiv(j.H, R);
+    CUtensorMap map;
+    p.use_tma = stream::encode_input_map(j, RB / 4, BR, &map) ? 1 : 0;
+    auto kern = morph_col_kernel<T, MODE, GX, GY>;
+    cudaError_t e = cudaSuccess;
+    const int occ = kernel_occupancy((const void*)kern, WPB * 32, SMEM, &e);
+    if (e != cudaSuccess) return e;
+    const int sms = device_sm_count();
+    const long items = (long)p.nstrips * p.nbands * j.batch;
+    const long ctas = std::max(1L, std::min((items + WPB - 1) / WPB, (long)sms * std::max(1, occ)));
+    kern<<<dim3((unsigned)ctas), WPB * 32, SMEM, j.stream>>>(p, map);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename T, int MODE, int GY>
+cudaError_t col_dispatch_x(const MorphJob& j, int R) {
+    switch (j.gx) {
+    case 0: return launch_col_variant<T, MODE, 0, GY>(j, R);
+    case 1: return launch_col_variant<T, MODE, 1, GY>(j, R);
+    case 2: return launch_col_variant<T, MODE, 2, GY>(j, R);
+    case 3: return launch_col_variant<T, MODE, 3, GY>(j, R);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <typename T, int MODE>
+cudaError_t col_dispatch(const MorphJob& j, int R) {
+    switch (j.gy) {
+    case 0: return col_dispatch_x<T, MODE, 0>(j, R);
+    case 1: return col_dispatch_x<T, MODE, 1>(j, R);
+    case 2: return col_dispatch_x<T, MODE, 2>(j, R);
+    case 3: return col_dispatch_x<T, MODE, 3>(j, R);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace col
+}  // namespace rmgpu

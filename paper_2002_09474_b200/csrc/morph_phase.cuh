@@ -553,15 +553,11 @@ cudaError_t launch_phase_variant(const MorphJob& j, int rh, int B, int q, int pf
     p.use_tma_out = encode_output_map(j, G::TW * (int)sizeof(T), chunk_rows(B), &omap) ? 1 : 0;
     const PPlan pl = make_pplan<T, HB>(B, q, pf);
     auto kern = morph_phase_kernel<T, MODE, VB, HB>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
+    cudaError_t e = cudaSuccess;
+    const int occ = kernel_occupancy((const void*)kern, PNT + 32, pl.total, &e);
     if (e != cudaSuccess) return e;
+    const int sms = device_sm_count();
     const long items = (long)cdiv(j.W, G::TW) * cdiv(j.H, rh) * j.batch;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PNT + 32, pl.total);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long ctas = std::max(1L, std::min(items, (long)sms * std::max(1, occ)));
     kern<<<dim3((unsigned)ctas), PNT + 32, pl.total, j.stream>>>(p, map, omap);
     count_launch();

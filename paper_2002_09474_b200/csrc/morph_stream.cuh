@@ -748,15 +748,11 @@ cudaError_t launch_stream_variant(const MorphJob& j, int rh, int B, int q, int p
     p.use_tma_out = encode_output_map(j, G::TW * (int)sizeof(T), B, &omap) ? 1 : 0;
     const Plan pl = make_plan<T, HB>(B, q, pf);
     auto kern = morph_stream_kernel<T, MODE, VB, HB>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
+    cudaError_t e = cudaSuccess;
+    const int occ = kernel_occupancy((const void*)kern, KG<T, VB, HB>::NTH, pl.total, &e);
     if (e != cudaSuccess) return e;
+    const int sms = device_sm_count();
     const long items = (long)cdiv(j.W, G::TW) * cdiv(j.H, rh) * j.batch;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, KG<T, VB, HB>::NTH, pl.total);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long ctas = std::max(1L, std::min(items, (long)sms * std::max(1, occ)));
     dim3 grid((unsigned)ctas, 1, 1);
     p.batch = j.batch;

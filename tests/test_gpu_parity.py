@@ -111,6 +111,33 @@ def test_random_medium_all_ops(gpu, restatement, dtype):
         assert np.array_equal(got, want), (c, w, h, wx, wy, op, border, bval)
 
 
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_small_window_fuzz_aligned(gpu, restatement, dtype):
+    # windows <= 7 on 16-byte aligned pitches: the register-streaming kernel (col_*) -- strip
+    # edges, image edges, widths around the 512-byte strip, short / tall images, both borders
+    rng = np.random.default_rng(4242 + np.dtype(dtype).itemsize)
+    mx = int(np.iinfo(dtype).max)
+    es = np.dtype(dtype).itemsize
+    widths = [1, 3, 4, 15, 16, 17, 255, 256, 257, 300, 508, 511, 512, 513, 516, 517, 1023, 1024, 1030, 1500]
+    seen = set()
+    for c in range(120):
+        w = int(widths[c % len(widths)]) if c < 60 else int(rng.integers(1, 1600))
+        h = int(rng.integers(1, 90))
+        wx, wy = (int(2 * v + 1) for v in rng.integers(0, 4, 2))
+        op = int(rng.integers(0, 2))
+        border = int(rng.integers(0, 2))
+        bval = int(rng.integers(0, mx + 1))
+        pad = (-w) % (16 // es) + int(rng.integers(0, 3)) * (16 // es)
+        img = restatement.generate(w, h, 9100 + c, dtype=dtype)
+        want = restatement.morph(img, wx, wy, op, border, bval)
+        got, dst = gpu_morph(gpu, img, wx, wy, op, border, bval, pad=pad, poison=0x5A)
+        assert np.array_equal(got, want), (c, w, h, wx, wy, op, border, bval, pad)
+        full = to_host_full(dst, w + pad)
+        assert np.all(full[:, w:] == 0xA5), ("padding written", c, w, h, wx, wy)
+        seen.add(gpu.plan_name(es, w, h, wx, wy, op).split("_")[0])
+    assert "col" in seen, seen
+
+
 @pytest.mark.parametrize("win", [(3, 3), (7, 7), (15, 15), (21, 21), (31, 31), (63, 63), (101, 101), (31, 1),
                                  (1, 31), (151, 5), (5, 151), (301, 301), (1001, 3)])
 def test_window_sweep(gpu, restatement, win):
