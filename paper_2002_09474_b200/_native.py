@@ -10,7 +10,7 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "librmgpu.so")
+LIB_PATH = os.environ.get("RMGPU_LIB_PATH") or os.path.join(_PKG, "librmgpu.so")  # override: tuning experiments
 HOSTLIB_PATH = os.path.join(_PKG, "librectmorph_b200.so")
 
 _P, _S, _I, _U, _U64 = C.c_void_p, C.c_size_t, C.c_int, C.c_uint, C.c_uint64

@@ -23,7 +23,8 @@ HOSTLIB = os.path.join(PKG, "librectmorph_b200.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + (["-DRMGPU_TRACE"] if os.environ.get("RMGPU_TRACE") else []) + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+NVCC_FLAGS = ARCH + (["-DRMGPU_TRACE"] if os.environ.get("RMGPU_TRACE") else []) + \
+    os.environ.get("RMGPU_EXTRA_DEFS", "").split() + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
                      "-I", os.path.join(ROOT, "include")]
 CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_fast.cu", "morph_fast_u8_min.cu", "morph_fast_u8_max.cu",

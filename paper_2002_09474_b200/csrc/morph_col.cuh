@@ -17,9 +17,18 @@ using stream::mbar_init;
 using stream::mbar_wait;
 using stream::tma_box;
 
-constexpr int WPB = 4;               // warps per CTA (independent pipelines sharing one smem block)
-constexpr int BR = 8;                // rows per TMA block
-constexpr int NS = 3;                // ring slots per warp
+#ifndef RM_COL_BR
+#define RM_COL_BR 8
+#endif
+#ifndef RM_COL_NS
+#define RM_COL_NS 3
+#endif
+#ifndef RM_COL_WPB
+#define RM_COL_WPB 4
+#endif
+constexpr int WPB = RM_COL_WPB;      // warps per CTA (independent pipelines sharing one smem block)
+constexpr int BR = RM_COL_BR;        // rows per TMA block
+constexpr int NS = RM_COL_NS;        // ring slots per warp
 constexpr int HALO = 16;             // halo bytes left / right of a strip row
 constexpr int SB = 512;              // strip bytes per row (32 lanes x 16 B)
 constexpr int RB = SB + 2 * HALO;    // bytes per staged row (544)
@@ -43,22 +52,68 @@ struct ColParams {
     int R;               // output rows per item
     int nstrips, nbands;
     int use_tma;
+    // item walk (host-computed): a warp visits items gw, gw + nwarps, ...; divisions by the strip
+    // count and the items per image use multiply-high magic numbers
+    int ds, dband, db;
+    uint32_t strip_m, img_m;
+    int strip_s, img_s;
 };
 
-// item n -> (image, band, strip); strips fastest so neighbouring warps share halo rows in L2
+// q = n / d for 0 <= n < 2^31 with host-computed (m, s): q = (umulhi(n, m) + n) >> s
+struct FastDivHost {
+    uint32_t m;
+    int s;
+    static FastDivHost make(uint32_t d) {
+        FastDivHost f;
+        int s = 0;
+        while ((1ull << s) < d) ++s;
+        f.s = s;
+        f.m = (uint32_t)((((1ull << s) - d) << 32) / d + 1);
+        return f;
+    }
+};
+__device__ __forceinline__ int fdiv(int n, uint32_t m, int s) {
+    return (int)((__umulhi((uint32_t)n, m) + (uint64_t)(uint32_t)n) >> s);
+}
+
+// Work item cursor: item n -> (image, band, strip), strips fastest so neighbouring warps share
+// halo rows in L2. A warp walks items gw, gw + nwarps, ... with mixed-radix increments (the
+// divisions happen once per warp).
+struct Cursor {
+    int b, band, strip;
+    __device__ __forceinline__ void init(const ColParams& p, int n) {
+        b = fdiv(n, p.img_m, p.img_s);
+        const int rem = n - b * p.nstrips * p.nbands;
+        band = fdiv(rem, p.strip_m, p.strip_s);
+        strip = rem - band * p.nstrips;
+    }
+    __device__ __forceinline__ void step(const ColParams& p) {
+        strip += p.ds;
+        int carry = 0;
+        if (strip >= p.nstrips) {
+            strip -= p.nstrips;
+            carry = 1;
+        }
+        band += p.dband + carry;
+        carry = 0;
+        if (band >= p.nbands) {
+            band -= p.nbands;
+            carry = 1;
+        }
+        b += p.db + carry;
+    }
+    __device__ __forceinline__ bool valid(const ColParams& p) const { return b < p.batch; }
+};
+
 struct CItem {
     int b, y0, x0, rows_out, nblk;
 };
 template <typename T, int GY>
-__device__ __forceinline__ CItem col_item(const ColParams& p, int n) {
+__device__ __forceinline__ CItem col_item(const ColParams& p, const Cursor& c) {
     CItem it;
-    const int per_img = p.nstrips * p.nbands;
-    it.b = n / per_img;
-    const int rem = n - it.b * per_img;
-    const int band = rem / p.nstrips;
-    const int strip = rem - band * p.nstrips;
-    it.y0 = band * p.R;
-    it.x0 = strip * (SB / (int)sizeof(T));
+    it.b = c.b;
+    it.y0 = c.band * p.R;
+    it.x0 = c.strip * (SB / (int)sizeof(T));
     it.rows_out = min(p.R, p.H - it.y0);
     it.nblk = (it.rows_out + 2 * GY + BR - 1) / BR;
     return it;
@@ -99,59 +154,33 @@ struct RowW<uint16_t> {
     static constexpr int N = 6;   // w0..w3, X0, X1
 };
 
-template <typename T, int MODE, int GX, int GY, bool EDGE>
+template <typename T, int MODE, int GX, int GY>
 struct ColCore {
     static constexpr int NW = RowW<T>::N;
     static constexpr int WV = 2 * GY + 1;
     static constexpr int sz = sizeof(T);
     static constexpr int PXL = 16 / sz;  // pixels per lane
 
-    // load one staged row into expanded words (+ border columns fixed in EDGE strips)
-    static __device__ __forceinline__ void load_row(const unsigned char* row, int lane, uint32_t* e,
-                                                    const uint32_t* sel, uint32_t fill_l, uint32_t fill_r,
-                                                    const ColParams& p, int x0) {
+    // load one staged row into expanded words
+    static __device__ __forceinline__ void load_row(const unsigned char* row, int lane, uint32_t* e) {
         const uint4 m = *reinterpret_cast<const uint4*>(row + HALO + lane * 16);
-        uint32_t w[4] = {m.x, m.y, m.z, m.w};
-        uint32_t x[2];
+        const uint32_t w[4] = {m.x, m.y, m.z, m.w};
         const int xo = lane == 0 ? HALO - 8 : HALO + SB;
         const uint2 xx = *reinterpret_cast<const uint2*>(row + xo);
         if constexpr (sz == 1) {
-            x[0] = lane == 0 ? xx.y : xx.x;  // left: bytes x0-4..x0-1; right: x0+512..x0+515
-        } else {
-            x[0] = xx.x;
-            x[1] = xx.y;
-        }
-        if constexpr (EDGE) {
-            uint32_t fl = fill_l, fr = fill_r;
-            if (p.cmode == 0) {
-                // replicate: the first / last image pixel of this row
-                if constexpr (sz == 1) {
-                    fl = row[HALO] * 0x01010101u;
-                    fr = row[HALO + min(p.W - 1 - x0, SB + 3)] * 0x01010101u;
-                } else {
-                    fl = *reinterpret_cast<const uint16_t*>(row + HALO) * 0x00010001u;
-                    fr = *reinterpret_cast<const uint16_t*>(row + HALO + min(p.W - 1 - x0, SB / 2 + 3) * 2) * 0x00010001u;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) w[k] = prmt(w[k], fr, sel[k]);
-            const uint32_t fx = lane == 0 ? fl : fr;
-            x[0] = prmt(x[0], fx, sel[4]);
-            if constexpr (sz == 2) x[1] = prmt(x[1], fx, sel[5]);
-        }
-        if constexpr (sz == 1) {
+            const uint32_t x = lane == 0 ? xx.y : xx.x;  // left: bytes x0-4..x0-1; right: x0+512..
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 e[k] = prmt(w[k], w[k], 0x2301);  // even pixels into the high bytes
                 e[4 + k] = w[k];                  // odd pixels already there
             }
-            e[8] = prmt(x[0], x[0], 0x2301);
-            e[9] = x[0];
+            e[8] = prmt(x, x, 0x2301);
+            e[9] = x;
         } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k) e[k] = w[k];
-            e[4] = x[0];
-            e[5] = x[1];
+            e[4] = xx.x;
+            e[5] = xx.y;
         }
     }
 
@@ -235,6 +264,43 @@ struct ColCore {
     }
 };
 
+// Ragged right edge: only the lane's first nbytes output bytes are inside the image.
+static __device__ __noinline__ void store_partial(uint8_t* d, uint4 out, int nbytes) {
+    if (nbytes <= 0) return;
+    const uint32_t ow[4] = {out.x, out.y, out.z, out.w};
+    for (int b = 0; b < nbytes; ++b) d[b] = (uint8_t)(ow[b >> 2] >> (8 * (b & 3)));
+}
+
+// Border strips: overwrite the staged out-of-image columns of one block in shared memory
+// (replicate: the row's first / last pixel; constant: the border value), so the row loop itself
+// has no border logic. Lane-parallel, border strips only.
+template <typename T>
+__device__ __forceinline__ void fix_block_columns(unsigned char* blk, int lane, int x0, int W, int cmode, uint32_t bv) {
+    constexpr int sz = sizeof(T);
+    if (x0 == 0) {  // 16 halo bytes left of column 0: 8 rows x 4 words = one word per lane
+        const int r = lane >> 2, wI = lane & 3;
+        unsigned char* row = blk + r * RB;
+        uint32_t f = bv;
+        if (cmode == 0) f = sz == 1 ? row[HALO] * 0x01010101u : *reinterpret_cast<const uint16_t*>(row + HALO) * 0x00010001u;
+        __syncwarp();
+        reinterpret_cast<uint32_t*>(row)[wI] = f;
+    }
+    const int start = HALO + (W - x0) * sz;  // first staged byte at column >= W
+    if (start < RB) {
+        const int wstart = (start + 3) >> 2;    // first whole word
+        for (int r = 0; r < BR; ++r) {
+            unsigned char* row = blk + r * RB;
+            uint32_t f = bv;
+            if (cmode == 0)
+                f = sz == 1 ? row[start - 1] * 0x01010101u : *reinterpret_cast<const uint16_t*>(row + start - 2) * 0x00010001u;
+            __syncwarp();
+            for (int i = start + lane; i < min(wstart * 4, RB); i += 32) row[i] = (uint8_t)(f >> (8 * (i & 3)));
+            for (int wI = wstart + lane; wI < RB / 4; wI += 32) reinterpret_cast<uint32_t*>(row)[wI] = f;
+        }
+    }
+    __syncwarp();
+}
+
 template <typename T, int MODE, int GX, int GY>
 __global__ void __launch_bounds__(WPB * 32)
 morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap) {
@@ -242,33 +308,36 @@ morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int PXL = 16 / sz;
     constexpr int SWPX = SB / sz;
     constexpr int WV = 2 * GY + 1;
+    constexpr int RING = WV == 1 ? 1 : (WV <= 4 ? 4 : 8);  // power of two dividing BR: compile-time slots
     constexpr int NW = RowW<T>::N;
+    using C = ColCore<T, MODE, GX, GY>;
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + wib * NS;
     unsigned char* ring = smem + HDR + wib * WARPB;
+    const int nwarps = gridDim.x * WPB;
+    const int gw = blockIdx.x * WPB + wib;
+    const int nitems = p.nstrips * p.nbands * p.batch;
+    if (gw >= nitems) return;
     if (lane == 0) {
         for (int k = 0; k < NS; ++k) mbar_init(&bars[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
-
-    const int nwarps = gridDim.x * WPB;
-    const int gw = blockIdx.x * WPB + wib;
-    const int nitems = p.nstrips * p.nbands * p.batch;
-    if (gw >= nitems) return;
     const uint32_t bv = sz == 1 ? (p.bval & 0xFF) * 0x01010101u : (p.bval & 0xFFFF) * 0x00010001u;
 
-    // ---- producer side (all lanes run it; lane 0 / lanes < BR issue) ----------------------------
-    int in_ = gw, ib = 0;  // next block to issue: item index, block within item
-    CItem iit = col_item<T, GY>(p, in_);
-    int iseq = 0;          // blocks issued
+    // ---- producer side (warp-collective; lane 0 / lanes < BR issue) -----------------------------
+    Cursor ic;
+    ic.init(p, gw);
+    const Cursor c0 = ic;
+    CItem iit = col_item<T, GY>(p, ic);
+    bool ivalid = true;
+    int ib = 0, islot = 0;
     auto issue = [&]() {
-        if (in_ >= nitems) return;
-        const int slot = iseq % NS;
-        unsigned char* dstb = ring + slot * SLOTB;
-        uint64_t* bar = &bars[slot];
+        if (!ivalid) return;
+        unsigned char* dstb = ring + islot * SLOTB;
+        uint64_t* bar = &bars[islot];
         const int yb = iit.y0 - GY + ib * BR;
         const int xb = iit.x0 * sz - HALO;  // byte column of the staged row start
         if (p.use_tma && yb >= p.row_lo && yb + BR <= p.row_hi) {
@@ -292,6 +361,7 @@ morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap) {
                 for (int c = lane; c < RB / 16; c += 32)
                     reinterpret_cast<uint4*>(dstb + r * RB)[c] = make_uint4(bv, bv, bv, bv);
             }
+            fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive_tx(bar, (uint32_t)(__popc(cp) * len));
             __syncwarp();
@@ -301,97 +371,66 @@ morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap) {
                          p.src + (size_t)iit.b * p.simg + (ptrdiff_t)yc * (ptrdiff_t)p.sp + c0, (uint32_t)len, bar);
             }
         }
-        ++iseq;
+        islot = islot + 1 == NS ? 0 : islot + 1;
         if (++ib == iit.nblk) {
             ib = 0;
-            in_ += nwarps;
-            if (in_ < nitems) iit = col_item<T, GY>(p, in_);
+            ic.step(p);
+            ivalid = ic.valid(p);
+            if (ivalid) iit = col_item<T, GY>(p, ic);
         }
     };
     for (int k = 0; k < NS; ++k) issue();
 
     // ---- consumer --------------------------------------------------------------------------------
-    int cseq = 0;  // blocks consumed
-    for (int n = gw; n < nitems; n += nwarps) {
-        const CItem it = col_item<T, GY>(p, n);
+    int cslot = 0;
+    uint32_t cpar = 0;
+    uint32_t E[RING][NW];
+    Cursor cc = c0;
+    for (; cc.valid(p); cc.step(p)) {
+        const CItem it = col_item<T, GY>(p, cc);
         const bool edge = it.x0 == 0 || it.x0 + SWPX + 4 > p.W;
-        uint8_t* dst = p.dst + (size_t)it.b * p.dimg + (size_t)it.x0 * sz + (size_t)lane * 16;
-        auto run = [&](auto edge_tag) {
-            constexpr bool EDGE = decltype(edge_tag)::value;
-            using C = ColCore<T, MODE, GX, GY, EDGE>;
-            // per-lane column selectors for the border strips: keep byte j, or take the fill word
-            uint32_t sel[6] = {0x3210, 0x3210, 0x3210, 0x3210, 0x3210, 0x3210};
-            uint32_t fill_l = bv, fill_r = bv;
-            int store_bytes = 16;
-            if constexpr (EDGE) {
-                auto selw = [&](int px0, int npx) {  // word of npx pixels starting at column px0
-                    uint32_t s = 0;
-                    for (int j = 0; j < 4; ++j) {
-                        const int px = px0 + j / sz;
-                        const bool ok = px >= 0 && px < p.W;
-                        s |= (uint32_t)(ok ? j : 4 + (j % sz)) << (4 * j);
+        const int store_bytes = max(0, min(16, (p.W - it.x0 - lane * PXL) * sz));
+        // destination of input row t: output row t - 2*GY
+        const ptrdiff_t dp = (ptrdiff_t)p.dp;
+        uint8_t* drow = p.dst + (size_t)it.b * p.dimg + (size_t)it.x0 * sz + (size_t)lane * 16 +
+                        (ptrdiff_t)(it.y0 - 2 * GY) * (ptrdiff_t)p.dp;
+        int o = -2 * GY;
+        for (int blk = 0; blk < it.nblk; ++blk) {
+            mbar_wait(&bars[cslot], cpar);
+            const unsigned char* rows = ring + cslot * SLOTB;
+            if (edge) fix_block_columns<T>(ring + cslot * SLOTB, lane, it.x0, p.W, p.cmode, bv);
+            // 8 rows; the row-validity test only in blocks with warm-up rows or rows past the band
+            auto block = [&](auto check_tag) {
+                constexpr bool CHECK = decltype(check_tag)::value;
+#pragma unroll
+                for (int r = 0; r < BR; ++r) {
+                    C::load_row(rows + r * RB, lane, E[r % RING]);
+                    if (!CHECK || (unsigned)(o + r) < (unsigned)it.rows_out) {
+                        uint32_t v[NW];
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) {
+                            uint32_t col[WV];
+#pragma unroll
+                            for (int k = 0; k < WV; ++k) col[k] = E[(r - k + 8 * RING) % RING][w];
+                            v[w] = opn<MODE, WV>(col);
+                        }
+                        const uint4 out = C::horizontal(v, lane);
+                        if (store_bytes == 16) *reinterpret_cast<uint4*>(drow) = out;
+                        else store_partial(drow, out, store_bytes);
                     }
-                    (void)npx;
-                    return s;
-                };
-                const int pxl = it.x0 + lane * PXL;
-                for (int k = 0; k < 4; ++k) sel[k] = selw(pxl + k * (4 / sz), 4 / sz);
-                const int xpx = lane == 0 ? it.x0 - 4 : it.x0 + SWPX;
-                sel[4] = selw(xpx, 4 / sz);
-                sel[5] = selw(xpx + 4 / sz, 4 / sz);
-                store_bytes = max(0, min(16, (p.W - pxl) * sz));
-            }
-            uint32_t E[WV][NW];
-            const int rows_in = it.rows_out + 2 * GY;
-            const unsigned char* rowp = nullptr;
-            int rib = BR;  // row index within the current block (BR = need a new block)
-            int o = -2 * GY;  // output row of the newest input row
-            for (int t0 = 0; t0 < rows_in; t0 += WV) {
-#pragma unroll
-                for (int j = 0; j < WV; ++j) {
-                    if (t0 + j < rows_in) {
-                        if (rib == BR) {
-                            const int slot = cseq % NS;
-                            mbar_wait(&bars[slot], (uint32_t)((cseq / NS) & 1));
-                            rowp = ring + slot * SLOTB;
-                            rib = 0;
-                        }
-                        C::load_row(rowp, lane, E[j], sel, fill_l, fill_r, p, it.x0);
-                        rowp += RB;
-                        ++rib;
-                        if (rib == BR || t0 + j == rows_in - 1) {
-                            // block fully read: hand the slot back to the producer
-                            ++cseq;
-                            __syncwarp();
-                            fence_async_smem();
-                            issue();
-                            rib = BR;
-                        }
-                        if (o >= 0) {
-                            uint32_t v[NW];
-#pragma unroll
-                            for (int w = 0; w < NW; ++w) {
-                                uint32_t col[WV];
-#pragma unroll
-                                for (int r = 0; r < WV; ++r) col[r] = E[r][w];
-                                v[w] = opn<MODE, WV>(col);
-                            }
-                            const uint4 out = C::horizontal(v, lane);
-                            uint8_t* d = dst + (size_t)(it.y0 + o) * p.dp;
-                            if (!EDGE || store_bytes == 16) {
-                                *reinterpret_cast<uint4*>(d) = out;
-                            } else if (store_bytes > 0) {
-                                const uint32_t ow[4] = {out.x, out.y, out.z, out.w};
-                                for (int bI = 0; bI < store_bytes; ++bI) d[bI] = (uint8_t)(ow[bI >> 2] >> (8 * (bI & 3)));
-                            }
-                        }
-                        ++o;
-                    }
+                    drow += dp;
                 }
-            }
-        };
-        if (edge) run(std::true_type{});
-        else run(std::false_type{});
+            };
+            if (o >= 0 && o + BR <= it.rows_out) block(std::false_type{});
+            else block(std::true_type{});
+            o += BR;
+            // block fully read by every lane: hand the slot back (the TMA refill is ordered after
+            // these generic-proxy reads by program order + the warp barrier)
+            __syncwarp();
+            cslot = cslot + 1 == NS ? 0 : cslot + 1;
+            cpar ^= cslot == 0;
+            issue();
+        }
     }
 }
 
@@ -424,6 +463,17 @@ cudaError_t launch_col_variant(const MorphJob& j, int R) {
     const int sms = device_sm_count();
     const long items = (long)p.nstrips * p.nbands * j.batch;
     const long ctas = std::max(1L, std::min((items + WPB - 1) / WPB, (long)sms * std::max(1, occ)));
+    const long nwarps = ctas * WPB;
+    const long per_img = (long)p.nstrips * p.nbands;
+    p.db = (int)(nwarps / per_img);
+    const long r2 = nwarps - (long)p.db * per_img;
+    p.dband = (int)(r2 / p.nstrips);
+    p.ds = (int)(r2 - (long)p.dband * p.nstrips);
+    const FastDivHost fs = FastDivHost::make((uint32_t)p.nstrips), fi = FastDivHost::make((uint32_t)per_img);
+    p.strip_m = fs.m;
+    p.strip_s = fs.s;
+    p.img_m = fi.m;
+    p.img_s = fi.s;
     kern<<<dim3((unsigned)ctas), WPB * 32, SMEM, j.stream>>>(p, map);
     count_launch();
     return cudaGetLastError();
