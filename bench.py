@@ -264,7 +264,199 @@ class Cfg1(Cfg2):
         return 2 * self.img.size
 
 
-WORKLOADS = {"cfg1": Cfg1, "cfg2": Cfg2}
+class Cfg4:
+    """512 u16 1024x1024 images (seed 4, stream = image index), opening 21x21 replicate, batch sharded
+    over the ranks (contiguous shards, no collective). One step = the rank's whole shard."""
+    name = "cfg4"
+    dtype = "u16"
+    graphable = False
+    N_IMAGES, SIZE, WIN = 512, 1024, 21
+
+    def __init__(self, dist: Dist):
+        from paper_2002_09474_b200.shard import batch_shard
+        self.dist = dist
+        self.first, self.count = batch_shard(self.N_IMAGES, dist.world, dist.rank)
+        self.img = generate(self.SIZE, self.SIZE, 4, self.first, np.uint16)  # CPU-leg sample image
+
+    def setup_device(self):
+        import torch
+        import paper_2002_09474_b200 as pkg
+        self.pkg = pkg
+        n = self.SIZE
+        self.src = torch.empty((self.count, n, n), dtype=torch.uint16, device="cuda")
+        self.dst = torch.empty_like(self.src)
+        for k in range(self.count):
+            pkg.generate_device(self.src[k], 4, self.first + k)
+        npx = self.count * n * n
+        self.ops = [(f"opening {self.WIN}x{self.WIN} x{self.count}", None, 4 * npx, npx)]
+
+    def launch(self, spec):
+        self.pkg.morph_batched_device(self.src, self.dst, self.WIN, self.WIN, OPEN)
+
+    def config(self):
+        return {"workload": f"cfg4: {self.N_IMAGES} x 1024x1024 u16 opening {self.WIN}x{self.WIN} (seed 4, "
+                            "stream = image index), batch sharded", "images_this_rank": self.count,
+                "border": "replicate", "l2": f"no flush: {self.count} x 2 MiB inputs >> L2 (G small)",
+                "parallelism": f"batch shards x{self.dist.world} (no collective)"}
+
+    def out_pixels_per_step(self):
+        return self.count * self.SIZE * self.SIZE
+
+    def e2e_setup(self):
+        import torch
+        self.h_in = self.src.cpu().pin_memory()
+        self.h_out = torch.empty_like(self.h_in).pin_memory()
+
+    def e2e_step(self):
+        import torch
+        d_in = self.h_in.to("cuda", non_blocking=True)
+        d_out = torch.empty_like(d_in)
+        self.pkg.morph_batched_device(d_in, d_out, self.WIN, self.WIN, OPEN)
+        self.h_out.copy_(d_out, non_blocking=True)
+        torch.cuda.synchronize()
+        nbytes = self.h_in.numel() * 2
+        return nbytes, nbytes
+
+    ref_port = True  # u16: the reference is u8-only; the CPU leg is the oracle restatement (SURVEY.md 8c)
+
+    def ref_step(self, R, nthreads, out):
+        R.morph(self.img, self.WIN, self.WIN, OPEN)
+        return self.SIZE * self.SIZE
+
+
+class Cfg5:
+    """32768^2 u8 (seed 5) dilation 63x63 replicate, split into G row bands; each step exchanges the
+    31-row halos with the neighbouring ranks (NCCL point-to-point) and computes the band."""
+    name = "cfg5"
+    dtype = "u8"
+    graphable = False
+    SIZE, WIN = 32768, 63
+
+    def __init__(self, dist: Dist):
+        from paper_2002_09474_b200.shard import band_plan
+        self.dist = dist
+        self.band = band_plan(self.SIZE, dist.world, dist.rank, self.WIN // 2)
+        self.img = generate(4096, 4096, 5)  # CPU-leg sample (a 4096^2 crop-sized image)
+
+    def setup_device(self):
+        import torch
+        import paper_2002_09474_b200 as pkg
+        self.pkg = pkg
+        b = self.band
+        full = torch.empty((self.SIZE, self.SIZE), dtype=torch.uint8, device="cuda")
+        pkg.generate_device(full, 5)
+        self.buf = full[b.in_y0:b.in_y0 + b.buffer_rows].clone()
+        del full
+        torch.cuda.empty_cache()
+        self.out = torch.empty((b.rows, self.SIZE), dtype=torch.uint8, device="cuda")
+        npx = b.rows * self.SIZE
+        self.ops = [(f"dilate {self.WIN}x{self.WIN} band {b.rows} rows (+{b.above}/{b.below} halo)", None, 2 * npx,
+                     npx)]
+
+    def launch(self, spec):
+        from paper_2002_09474_b200.shard import exchange_halos, morph_band
+        if self.dist.world > 1:
+            exchange_halos(self.buf, self.band, self.dist.world, self.dist.rank, self.WIN // 2, dist=self.dist.pg)
+        morph_band(self.buf, self.out, self.band, self.WIN, self.WIN, DILATE)
+
+    def config(self):
+        return {"workload": f"cfg5: {self.SIZE}x{self.SIZE} u8 dilate {self.WIN}x{self.WIN} (seed 5), row bands",
+                "band_rows_this_rank": self.band.rows, "halo_rows": [self.band.above, self.band.below],
+                "border": "replicate", "l2": "no flush: 1 GiB image >> L2",
+                "parallelism": f"row bands x{self.dist.world}, {self.WIN // 2}-row halo exchange per step "
+                               "(NCCL send/recv)"}
+
+    def out_pixels_per_step(self):
+        return self.band.rows * self.SIZE
+
+    def e2e_setup(self):
+        import torch
+        self.h_in = self.buf.cpu().pin_memory()
+        self.h_out = torch.empty_like(self.out, device="cpu").pin_memory()
+
+    def e2e_step(self):
+        import torch
+        self.buf.copy_(self.h_in, non_blocking=True)
+        self.launch(None)
+        self.h_out.copy_(self.out, non_blocking=True)
+        torch.cuda.synchronize()
+        return self.h_in.numel(), self.h_out.numel()
+
+    def ref_step(self, R, nthreads, out):
+        R.morph(self.img, self.WIN, self.WIN, DILATE, nthreads=nthreads, out=out)
+        return self.img.size
+
+
+class Cfg3:
+    """Standalone transposes: 8192^2 u8 and u16 images, 2^24 8x8 and 2^24 16x16 u8 tiles in place."""
+    name = "cfg3"
+    dtype = "u8/u16"
+    graphable = True
+    NB = 4
+
+    def __init__(self, dist: Dist):
+        self.dist = dist
+        self.img = generate(2048, 2048, 3)
+
+    def setup_device(self):
+        import torch
+        import paper_2002_09474_b200 as pkg
+        self.pkg = pkg
+        n = 8192
+        self.a8 = torch.empty((n, n), dtype=torch.uint8, device="cuda")
+        self.a16 = torch.empty((n, n), dtype=torch.uint16, device="cuda")
+        pkg.generate_device(self.a8, 3)
+        pkg.generate_device(self.a16, 30)
+        self.t8 = torch.empty_like(self.a8)
+        self.t16 = torch.empty_like(self.a16)
+        self.tiles8 = torch.empty((1 << 24) * 64, dtype=torch.uint8, device="cuda")
+        self.tiles16 = torch.empty((1 << 24) * 256, dtype=torch.uint8, device="cuda")
+        pkg.generate_device(self.tiles8.view(1 << 14, -1), 31)
+        pkg.generate_device(self.tiles16.view(1 << 16, -1), 32)
+        self.cursor = 0
+        e = n * n
+        self.ops = [("transpose 8192^2 u8", "t8", 2 * e, e), ("transpose 8192^2 u16", "t16", 4 * e, e),
+                    ("2^24 tiles 8x8 u8 in place", "k8", 2 * (1 << 24) * 64, (1 << 24) * 64),
+                    ("2^24 tiles 16x16 u8 in place", "k16", 2 * (1 << 24) * 256, (1 << 24) * 256)]
+
+    def launch(self, spec):
+        if spec == "t8":
+            self.pkg.transpose_device(self.a8, self.t8)
+        elif spec == "t16":
+            self.pkg.transpose_device(self.a16, self.t16)
+        elif spec == "k8":
+            self.pkg.transpose_tiles_device(self.tiles8, 8)
+        else:
+            self.pkg.transpose_tiles_device(self.tiles16, 16)
+
+    def config(self):
+        return {"workload": "cfg3: transpose 8192^2 u8 + 8192^2 u16, 2^24 8x8 + 2^24 16x16 u8 tiles in place",
+                "unit_note": "value counts transposed elements (Gelem/s)", "l2": "no flush: buffers >> L2",
+                "parallelism": f"replicas x{self.dist.world}"}
+
+    def out_pixels_per_step(self):
+        return sum(o[3] for o in self.ops)
+
+    def e2e_setup(self):
+        import torch
+        self.h_in = self.a8.cpu().pin_memory()
+        self.h_out = torch.empty_like(self.h_in).pin_memory()
+
+    def e2e_step(self):
+        import torch
+        d = self.h_in.to("cuda", non_blocking=True)
+        o = torch.empty_like(d)
+        self.pkg.transpose_device(d, o)
+        self.h_out.copy_(o, non_blocking=True)
+        torch.cuda.synchronize()
+        return self.h_in.numel(), self.h_out.numel()
+
+    def ref_step(self, R, nthreads, out):
+        R.transpose_image(self.img, nthreads=nthreads)
+        return self.img.size
+
+
+WORKLOADS = {"cfg1": Cfg1, "cfg2": Cfg2, "cfg3": Cfg3, "cfg4": Cfg4, "cfg5": Cfg5}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -275,11 +467,12 @@ def run_reference_arm(args, dist: Dist):
         return 0
     import oracle
     wl = WORKLOADS[args.workload](dist)
-    if not oracle.Reference.available():
+    port = getattr(wl, "ref_port", False)
+    if not port and not oracle.Reference.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/librmref.so not built"}))
         return 0
-    R = oracle.reference()
-    nthreads = os.cpu_count() or 1
+    R = oracle.restatement() if port else oracle.reference()
+    nthreads = 1 if port else (os.cpu_count() or 1)
     out = np.empty_like(wl.img)
     for _ in range(args.warmup):
         wl.ref_step(R, nthreads, out)
@@ -293,23 +486,27 @@ def run_reference_arm(args, dist: Dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype,
             "data": "synthetic (seeded generator, SURVEY.md 8d)", "config": wl.config(),
-            "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": nthreads, "kind": "reference",
-                             "sample": f"full workload per step; reference rectmorph (oracle/_ref, -O3, "
-                                       f"DispatchConfig paper 69/59) on {nthreads} threads via row bands"},
+            "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": nthreads,
+                             "kind": "port" if port else "reference",
+                             "sample": (f"one {wl.name} image per step through the oracle restatement (u16 has no "
+                                        "reference implementation), 1 thread") if port else
+                                       (f"{wl.name} sample per step; reference rectmorph (oracle/_ref, -O3, "
+                                        f"DispatchConfig paper 69/59) on {nthreads} threads via row bands")},
             "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
 def cpu_baseline(wl) -> dict | None:
+    port = getattr(wl, "ref_port", False)
     try:
         import oracle
-        if not oracle.Reference.available():
+        if not port and not oracle.Reference.available():
             return None
-        R = oracle.reference()
+        R = oracle.restatement() if port else oracle.reference()
     except Exception:
         return None
-    nthreads = os.cpu_count() or 1
+    nthreads = 1 if port else (os.cpu_count() or 1)
     out = np.empty_like(wl.img)
     wl.ref_step(R, nthreads, out)  # warm
     t0 = time.perf_counter()
@@ -321,9 +518,10 @@ def cpu_baseline(wl) -> dict | None:
         if time.perf_counter() - t0 > 3.0 or reps >= 5:
             break
     dt = time.perf_counter() - t0
-    return {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": nthreads, "kind": "reference",
-            "sample": f"{reps} full step(s) of {wl.name} through the reference rectmorph (oracle/_ref) on "
-                      f"{nthreads} host threads (row bands + halo), paper DispatchConfig"}
+    return {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": nthreads, "kind": "port" if port else "reference",
+            "sample": f"{reps} x {wl.name} CPU sample ({px // max(reps, 1)} output px each) through "
+                      + ("the oracle restatement (u16: no reference), 1 thread" if port else
+                         f"the reference rectmorph (oracle/_ref) on {nthreads} host threads (row bands + halo)")}
 
 
 def main(argv=None):
@@ -343,6 +541,7 @@ def main(argv=None):
 
     nops = len(wl.ops)
     ngraphs = max(1, getattr(wl, "NB", nops) // nops)
+    use_graphs = not args.eager and getattr(wl, "graphable", True)
 
     def eager_step():
         for (_, spec, _, _) in wl.ops:
@@ -355,7 +554,7 @@ def main(argv=None):
     # One CUDA graph per step (16 kernel nodes; one graph per rotating-buffer assignment), so the
     # timed region measures the kernels, not Python/ctypes launch latency.
     graphs, glaunch = [], 0
-    if not args.eager:
+    if use_graphs:
         cap = torch.cuda.Stream()
         wl.cursor = 0
         for _ in range(ngraphs):
@@ -405,7 +604,7 @@ def main(argv=None):
     per_window = []
     tot_b = tot_t = 0.0
     for (label, spec, nbytes, npx) in wl.ops:
-        nb = getattr(wl, "NB", 1)
+        nb = getattr(wl, "NB", 1) if graphs else 3
         wl.cursor = 0
         if graphs:
             g = torch.cuda.CUDAGraph()
@@ -470,7 +669,7 @@ def main(argv=None):
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": wl.dtype,
                 "data": "synthetic (seeded counter-based generator, SURVEY.md 8d; no dataset named)",
-                "config": dict(wl.config(), launch="eager" if args.eager else "one CUDA graph per step (16 kernel nodes)"),
+                "config": dict(wl.config(), launch=f"one CUDA graph per step ({glaunch} kernel nodes)" if graphs else "eager"),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
                              "kernel": "fused separable morph (all launches of the step)",
