@@ -90,7 +90,7 @@ bool choose(const MorphJob& j, Choice* c) {
             const int occ = std::max(1, std::min(8, (228 * 1024) / (t + 1024)));
             pf = cand;
             total = t;
-            if ((long)cand * blk * occ >= 64 * 1024) break;
+            if ((long)cand * blk * occ >= 48 * 1024) break;
         }
     }
     c->pf = pf;

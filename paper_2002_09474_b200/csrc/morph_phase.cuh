@@ -74,7 +74,7 @@ __device__ __forceinline__ int emitting_chunks(const Item& it, int KB) {
 }
 
 template <typename T, int MODE, int VB, int HB>
-__global__ void __launch_bounds__(PNT + 32)
+__global__ void __launch_bounds__(PNT + 32, 2)
 morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tmap,
                    const __grid_constant__ CUtensorMap omap) {
     using G = SG<T>;

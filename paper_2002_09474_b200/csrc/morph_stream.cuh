@@ -167,7 +167,7 @@ template <typename T, int HB>
 struct HG {
     static constexpr int sz = sizeof(T);
     static constexpr int TW = SG<T>::TW;
-    static constexpr int GXMAX = HB <= 7 ? (HB - 1) / 2 : (HB == 8 ? (sz == 1 ? 48 : 24) : (sz == 1 ? 112 : 56));
+    static constexpr int GXMAX = HB <= 7 ? (HB - 1) / 2 : (HB == 8 ? (sz == 1 ? 48 : 24) : (sz == 1 ? 64 : 32));
     static constexpr int RP = ((TW * sz + 2 * GXMAX * sz + 31) / 16) * 16;  // ring row pitch (bytes)
     static constexpr int NCH = (TW + 2 * GXMAX + 7) / 8 + 2;                // 8-column chunks (+ slack)
     static constexpr int NCHP = NCH | 1;                                     // odd: conflict-free lanes
