@@ -53,16 +53,20 @@ bool choose(const MorphJob& j, Choice* c) {
     } else {
         double best = 1e30;
         c->vb = 0;
-        for (int B : {8, 12, 16, 20, 24, 28, 32}) {
+        // halo class first (it sets the ring row pitch), then the block size: min/max per output
+        // ~ 3 + (2r + q)/B (+ per-block overhead 6/B), divided by the CTAs that fit per SM (max 2)
+        const int hb0 = j.gx <= 3 ? 2 * j.gx + 1 : (j.gx <= stream_gxmax(j.elem, 8) ? 8 : 9);
+        for (int B : {8, 12, 16, 20, 24, 28}) {
             if (B > w1) continue;
             const int q = w1 / B, r = w1 - q * B;
-            if (q > QMAX) continue;
-            // min/max per output ~ 3 + (r + q)/B; small blocks pay per-block overhead, the tail
-            // rows are a serial loop
-            const double cost = 3.0 + double(2 * r + q) / B + 6.0 / B;
+            if (q > QMAX || (r != 0 && r != 2)) continue;  // tail length is a compile-time 0 or 2
+            const int t = j.elem == 1 ? phase_smem<uint8_t>(hb0, B, q, 2) : phase_smem<uint16_t>(hb0, B, q, 2);
+            if (t > 220 * 1024) continue;
+            const int occ = std::max(1, std::min(2, (228 * 1024) / (t + 1024)));
+            const double cost = (3.0 + double(2 * r + q) / B + 6.0 / B) / occ;
             if (cost < best - 1e-9) {
                 best = cost;
-                c->vb = B;
+                c->vb = B + (r ? 100 : 0);
                 c->B = B;
                 c->q = q;
             }
@@ -84,10 +88,13 @@ bool choose(const MorphJob& j, Choice* c) {
         pf = std::max(1, atoi(e));
         total = smem_of(pf);
     } else {
+        // deepest prefetch (up to ~48 KB in flight per SM) that keeps the occupancy of PF = 2
+        const int occ_ref = std::max(1, std::min(8, (228 * 1024) / (smem_of(2) + 1024)));
         for (int cand = 1; cand <= 16; ++cand) {
             const int t = smem_of(cand);
             if (t > 220 * 1024) break;
             const int occ = std::max(1, std::min(8, (228 * 1024) / (t + 1024)));
+            if (cand > 2 && occ < occ_ref) break;
             pf = cand;
             total = t;
             if ((long)cand * blk * occ >= 48 * 1024) break;
@@ -133,7 +140,7 @@ const char* plan_name(const MorphJob& j) {
     Choice c;
     if (!choose(k, &c)) return nullptr;
     snprintf(buf, sizeof(buf), "phase_%s_v%s%d_h%s%d_rh%d_pf%d_smem%dK", j.elem == 1 ? "u8" : "u16",
-             c.vb <= 7 ? "d" : "b", c.vb, c.hb <= 7 ? "d" : "b", c.hb, c.rh, c.pf, c.smem / 1024);
+             c.vb <= 7 ? "d" : "b", c.vb % 100, c.hb <= 7 ? "d" : "b", c.hb, c.rh, c.pf, c.smem / 1024);
     return buf;
 }
 

@@ -82,7 +82,8 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
     constexpr int GR = G::GR, TW = G::TW, ESZ = G::ESZ;
     constexpr int sz = sizeof(T);
     constexpr bool VDIRECT = VB <= 7;
-    constexpr int B = VDIRECT ? VCH : VB;      // rows per block (TMA box)
+    constexpr int VR = VB >= 100 ? 2 : 0;      // block mode: tail rows r = w1 mod B (compile-time 0 or 2)
+    constexpr int B = VDIRECT ? VCH : VB % 100;  // rows per block (TMA box)
     constexpr int CH = chunk_rows(B);          // rows per chunk (horizontal hand-off)
     constexpr int KB = CH / B;                 // blocks per chunk
     constexpr int NGC = CH / GR;               // row groups per chunk
@@ -94,7 +95,7 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
 
     const int w1 = 2 * p.gy, w1x = 2 * p.gx;
     const int q = VDIRECT ? 0 : w1 / B;
-    const int r = VDIRECT ? w1 : w1 - q * B;
+    const int r = VDIRECT ? w1 : VR;
     const int s = r & 3;
     const int PF = p.pf;
     const PPlan pl = make_pplan<T, HB>(B, q, PF);
@@ -222,7 +223,7 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
                     --stores_left;
                 }
             }
-            if (!did) __nanosleep(40);
+            if (!did && p.sleep_ns) __nanosleep(p.sleep_ns);
         }
         if (lane == 0) {
             if (pending >= 0) mbar_arrive(&oempty[pending]);
@@ -548,6 +549,8 @@ cudaError_t launch_phase_variant(const MorphJob& j, int rh, int B, int q, int pf
     p.batch = j.batch;
     p.trace = g_trace;
     p.trace_cta = g_trace_cta;
+    static const int sleep_ns = getenv("RMGPU_PHASE_SLEEP") ? atoi(getenv("RMGPU_PHASE_SLEEP")) : 100;
+    p.sleep_ns = sleep_ns;
     CUtensorMap map, omap;
     p.use_tma = encode_input_map(j, HG<T, HB>::RP / 4, B, &map) ? 1 : 0;
     p.use_tma_out = encode_output_map(j, G::TW * (int)sizeof(T), chunk_rows(B), &omap) ? 1 : 0;
@@ -564,7 +567,7 @@ cudaError_t launch_phase_variant(const MorphJob& j, int rh, int B, int q, int pf
     return cudaGetLastError();
 }
 
-#define RM_PHASE_V(X) X(1) X(3) X(5) X(7) X(8) X(12) X(16) X(20) X(24) X(28) X(32)
+#define RM_PHASE_V(X) X(1) X(3) X(5) X(7) X(8) X(12) X(16) X(20) X(24) X(28) X(108) X(112) X(116) X(120) X(124) X(128)
 #define RM_PHASE_H(X) X(1) X(3) X(5) X(7) X(8) X(9)
 
 template <typename T, int MODE, int VB>
