@@ -266,6 +266,7 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
         const Item it = make_item<T>(p, item_at(n), nstrips, nrowb, B, w1, s);
         uint8_t* dst = p.dst + (size_t)it.b * p.dimg;
         const bool real = tid < it.nwv;
+        const bool vwarp = warp * 32 < it.nwv;  // warp-uniform: any real column word in this warp
         const int t = real ? tid : it.nwv - 1;
         int load_off = 0;
         uint32_t nib = 0;
@@ -310,11 +311,15 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
             for (int kb = 0; kb < KB; ++kb) {
                 const int L = c0 + kb;
                 if (L > it.Lend) break;
+                const bool emit = L >= it.Lf;
+                emit_any |= emit;
+                if (!vwarp) {  // warp holds no column word of this strip: only track the ring
+                    advance();
+                    continue;
+                }
                 if (warp == 0 && kb == 0) RM_TRACE(tci * 8 + 1);
                 mbar_wait(&full[sL], (uint32_t)ph);
                 if (warp == 0 && kb == 0) RM_TRACE(tci * 8 + 2);
-                const bool emit = L >= it.Lf;
-                emit_any |= emit;
                 const unsigned char* lead = sbase(sL);
                 uint32_t grp[GR];
                 auto flush = [&](int m0) {
