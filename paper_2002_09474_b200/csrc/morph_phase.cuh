@@ -143,87 +143,82 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
         int stores_left = 0;
         for (int n = 0; item_at(n) < nitems; ++n)
             stores_left += emitting_chunks(make_item<T>(p, item_at(n), nstrips, nrowb, B, w1, s), KB);
+        // Event-ordered loop: the compute warps release ring slots and then publish chunk c's
+        // output (OFULL) at the end of every emitting chunk, so waiting (suspended) on OFULL[c]
+        // guarantees every slot freed so far is already released: issue the store, then refill
+        // all free slots. No polling.
         int sc = 0, pending = -1;
-        while (pvalid || stores_left > 0) {
-            bool did = false;
-            if (pvalid) {
-                int ready = 1;
-                if (lane == 0 && puse > 0) ready = mbar_test(&empty[pslot], (uint32_t)((puse - 1) & 1));
-                ready = __shfl_sync(0xffffffffu, ready, 0);
-                if (ready) {
-                    did = true;
-                    const int slot = pslot;
-                    unsigned char* base = ring + (size_t)slot * SLOT;
-                    const int yb = pit.y_first + s + pk * B;
-                    if (p.use_tma && yb >= p.row_lo && yb + B <= p.row_hi) {
-                        if (lane == 0) {
-                            mbar_arrive_tx(&full[slot], (uint32_t)(B * RP));
-                            tma_box(base, &tmap, pit.xs_b / 4, yb - p.row_lo, pit.b, &full[slot]);
-                        }
-                    } else {
-                        const uint8_t* src = p.src + (size_t)pit.b * p.simg;
-                        const int y = yb + lane;
-                        const bool inrow = lane < B;
-                        const bool outside = p.cmode && (y < p.row_lo || y >= p.row_hi);
-                        const unsigned cp = __ballot_sync(0xffffffffu, inrow && !outside);
-                        unsigned fillm = __ballot_sync(0xffffffffu, inrow && outside);
-                        while (fillm) {
-                            const int m = __ffs(fillm) - 1;
-                            fillm &= fillm - 1;
-                            const uint32_t bw = sz == 1 ? bv * 0x01010101u : bv * 0x00010001u;
-                            uint4* row = reinterpret_cast<uint4*>(base + (size_t)m * RP);
-                            for (int c = lane; c < RP / 16; c += 32) row[c] = make_uint4(bw, bw, bw, bw);
-                        }
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_tx(&full[slot], (uint32_t)(__popc(cp) * pit.copy_len));
-                        __syncwarp();
-                        if (inrow && !outside) {
-                            const int yc = min(max(y, p.row_lo), p.row_hi - 1);
-                            bulk_g2s(base + (size_t)lane * RP + (pit.cb0 - pit.xs_b),
-                                     src + (ptrdiff_t)yc * (ptrdiff_t)p.sp + pit.cb0, (uint32_t)pit.copy_len,
-                                     &full[slot]);
-                        }
-                    }
-                    if (++pslot == NSB) {
-                        pslot = 0;
-                        ++puse;
-                    }
-                    if (++pk > pit.Lend) {
-                        ++pn;
-                        pk = -1;
-                        pvalid = item_at(pn) < nitems;
-                        if (pvalid) pit = make_item<T>(p, item_at(pn), nstrips, nrowb, B, w1, s);
-                    }
+        auto issue_load = [&]() {
+            const int slot = pslot;
+            unsigned char* base = ring + (size_t)slot * SLOT;
+            const int yb = pit.y_first + s + pk * B;
+            if (p.use_tma && yb >= p.row_lo && yb + B <= p.row_hi) {
+                if (lane == 0) {
+                    mbar_arrive_tx(&full[slot], (uint32_t)(B * RP));
+                    tma_box(base, &tmap, pit.xs_b / 4, yb - p.row_lo, pit.b, &full[slot]);
+                }
+            } else {
+                const uint8_t* src = p.src + (size_t)pit.b * p.simg;
+                const int y = yb + lane;
+                const bool inrow = lane < B;
+                const bool outside = p.cmode && (y < p.row_lo || y >= p.row_hi);
+                const unsigned cp = __ballot_sync(0xffffffffu, inrow && !outside);
+                unsigned fillm = __ballot_sync(0xffffffffu, inrow && outside);
+                while (fillm) {
+                    const int m = __ffs(fillm) - 1;
+                    fillm &= fillm - 1;
+                    const uint32_t bw = sz == 1 ? bv * 0x01010101u : bv * 0x00010001u;
+                    uint4* row = reinterpret_cast<uint4*>(base + (size_t)m * RP);
+                    for (int c = lane; c < RP / 16; c += 32) row[c] = make_uint4(bw, bw, bw, bw);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive_tx(&full[slot], (uint32_t)(__popc(cp) * pit.copy_len));
+                __syncwarp();
+                if (inrow && !outside) {
+                    const int yc = min(max(y, p.row_lo), p.row_hi - 1);
+                    bulk_g2s(base + (size_t)lane * RP + (pit.cb0 - pit.xs_b),
+                             src + (ptrdiff_t)yc * (ptrdiff_t)p.sp + pit.cb0, (uint32_t)pit.copy_len,
+                             &full[slot]);
                 }
             }
-            if (stores_left > 0) {
-                const int ob = sc & 1;
-                int ready = 0;
-                if (lane == 0) ready = mbar_test(&ofull[ob], (uint32_t)((sc >> 1) & 1));
-                ready = __shfl_sync(0xffffffffu, ready, 0);
-                if (ready) {
-                    did = true;
-                    if (lane == 0) {
-                        // the previous store has had a whole chunk to read its buffer: release it
-                        if (pending >= 0) {
-                            bulk_wait_read0();
-                            mbar_arrive(&oempty[pending]);
-                            pending = -1;
-                        }
-                        const int4 d = sdesc[ob];
-                        if (d.w) {
-                            tma_store_box(&omap, d.x, d.y, d.z, outbase + (size_t)ob * CH * OUTP);
-                            bulk_commit();
-                            pending = ob;
-                        } else {
-                            mbar_arrive(&oempty[ob]);  // copied by the compute warps already
-                        }
-                    }
-                    ++sc;
-                    --stores_left;
+            if (++pslot == NSB) {
+                pslot = 0;
+                ++puse;
+            }
+            if (++pk > pit.Lend) {
+                ++pn;
+                pk = -1;
+                pvalid = item_at(pn) < nitems;
+                if (pvalid) pit = make_item<T>(p, item_at(pn), nstrips, nrowb, B, w1, s);
+            }
+        };
+        auto slot_free = [&]() {
+            int ready = 1;
+            if (lane == 0 && puse > 0) ready = mbar_test(&empty[pslot], (uint32_t)((puse - 1) & 1));
+            return __shfl_sync(0xffffffffu, ready, 0) != 0;
+        };
+        while (pvalid && slot_free()) issue_load();  // prologue: the first NSB blocks
+        for (; stores_left > 0; --stores_left, ++sc) {
+            const int ob = sc & 1;
+            mbar_wait(&ofull[ob], (uint32_t)((sc >> 1) & 1));
+            if (lane == 0) {
+                // the previous store has had a whole chunk to read its buffer: release it
+                if (pending >= 0) {
+                    bulk_wait_read0();
+                    mbar_arrive(&oempty[pending]);
+                    pending = -1;
+                }
+                const int4 d = sdesc[ob];
+                if (d.w) {
+                    tma_store_box(&omap, d.x, d.y, d.z, outbase + (size_t)ob * CH * OUTP);
+                    bulk_commit();
+                    pending = ob;
+                } else {
+                    mbar_arrive(&oempty[ob]);  // copied by the compute warps already
                 }
             }
-            if (!did && p.sleep_ns) __nanosleep(p.sleep_ns);
+            __syncwarp();
+            while (pvalid && slot_free()) issue_load();
         }
         if (lane == 0) {
             if (pending >= 0) mbar_arrive(&oempty[pending]);
@@ -519,13 +514,14 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
                 }
                 bar_sync(BAR_C, PNT);  // copy finished: the producer may hand the buffer back
             }
+            // blocks no iteration after this chunk reads: everything below seq (g_last - q) of this
+            // item, or the whole item when it is finished -- released BEFORE the chunk is published,
+            // the producer refills slots right after it sees OFULL
+            release_below(item_done ? g_last + 1 : g_last - q);
             if (tid == 0) {
                 sdesc[ob] = make_int4(it.x0 * sz, it.y0 + oC, it.b, full_chunk ? 1 : 0);
                 mbar_arrive(&ofull[ob]);
             }
-            // blocks no iteration after this chunk reads: everything below seq (g_last - q) of this
-            // item, or the whole item when it is finished
-            release_below(item_done ? g_last + 1 : g_last - q);
             ++chunk;
         }
     }
