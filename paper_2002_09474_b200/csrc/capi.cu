@@ -171,6 +171,22 @@ int check_op_border(int op, int border, unsigned bval, int elem) {
     return RMGPU_OK;
 }
 
+// Scratch images (compound ops, two-pass fallback) come from the device's default stream-ordered
+// pool; keep freed blocks cached so repeated calls do not return memory to the driver.
+void keep_pool_cached() {
+    static std::atomic<unsigned long long> done{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    const unsigned long long bit = 1ull << dev;
+    if (done.load(std::memory_order_relaxed) & bit) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.fetch_or(bit, std::memory_order_relaxed);
+}
+
 // One erode / dilate / gradient over the job's rows. Window-1 axes are a copy
 // (separable.cpp:66,88); a 1x1 gradient is all zeros.
 int run_single(MorphJob j) {
@@ -212,6 +228,7 @@ int run_single(MorphJob j) {
     const size_t tmp_img = tmp_pitch * (size_t)j.H;
     const int nbuf = j.mode == rmgpu::MODE_GRAD ? 3 : 1;
     void* tmp = nullptr;
+    keep_pool_cached();
     RM_CUDA(cudaMallocAsync(&tmp, tmp_img * j.batch * nbuf, j.stream));
     auto run_pair = [&](int mode, void* out, size_t out_pitch, size_t out_img) -> int {
         MorphJob v = j;
@@ -288,6 +305,7 @@ int run_morph(const void* src, size_t sp, size_t simg, void* dst, size_t dp, siz
     const size_t tp = (row_bytes + 255) & ~size_t(255);
     const size_t timg = tp * (size_t)IH;
     void* tmp = nullptr;
+    keep_pool_cached();
     RM_CUDA(cudaMallocAsync(&tmp, timg * batch, stream));
     MorphJob a = j;
     a.mode = op == RMGPU_OPEN ? rmgpu::MODE_MIN : rmgpu::MODE_MAX;
