@@ -70,6 +70,108 @@ transpose_image_kernel(const T* __restrict__ src, size_t sp, T* __restrict__ dst
 }
 
 // ------------------------------------------------------------------------------------------
+// Register butterfly: a group of lanes (16 for u8, 8 for u16) each holding one 16-byte row of a
+// 16x16 u8 / 8x8 u16 block ends up holding one column (= one row of the transposed block).
+// Stage s (lane mask): lanes with (lane & s) == 0 keep the left half of every 2s-column block
+// and receive the partner's left half into the right half; the others keep the right half.
+// ------------------------------------------------------------------------------------------
+template <int ELEM>  // 1 = u8 16x16 (masks 8,4,2,1), 2 = u16 8x8 (masks 4,2,1)
+__device__ __forceinline__ void butterfly_rows(uint32_t (&w)[4], int lane) {
+    constexpr int TOP = ELEM == 1 ? 8 : 4;
+    {   // 2-word blocks
+        const bool lo = !(lane & TOP);
+        const uint32_t s0 = lo ? w[2] : w[0], s1 = lo ? w[3] : w[1];
+        const uint32_t r0 = __shfl_xor_sync(0xffffffffu, s0, TOP), r1 = __shfl_xor_sync(0xffffffffu, s1, TOP);
+        if (lo) { w[2] = r0; w[3] = r1; } else { w[0] = r0; w[1] = r1; }
+    }
+    {   // 1-word blocks
+        const bool lo = !(lane & (TOP / 2));
+        const uint32_t s0 = lo ? w[1] : w[0], s1 = lo ? w[3] : w[2];
+        const uint32_t r0 = __shfl_xor_sync(0xffffffffu, s0, TOP / 2), r1 = __shfl_xor_sync(0xffffffffu, s1, TOP / 2);
+        if (lo) { w[1] = r0; w[3] = r1; } else { w[0] = r0; w[2] = r1; }
+    }
+    {   // half-word blocks
+        const uint32_t sel = (lane & (TOP / 4)) ? 0x3276u : 0x5410u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = prmt(w[k], __shfl_xor_sync(0xffffffffu, w[k], TOP / 4), sel);
+    }
+    if constexpr (ELEM == 1) {  // bytes
+        const uint32_t sel = (lane & 1) ? 0x3715u : 0x6240u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = prmt(w[k], __shfl_xor_sync(0xffffffffu, w[k], 1), sel);
+    }
+}
+
+// Contiguous 16x16 u8 tiles (cfg3) / 8x8 u16 tiles: a warp moves 512 contiguous bytes per step
+// (2 u8 tiles / 4 u16 tiles, one 16-byte row per lane), transposes them with the register
+// butterfly and writes them back in place: fully coalesced 128-bit loads and stores.
+template <int ELEM>
+__global__ void __launch_bounds__(256)
+tiles_warp_kernel(uint8_t* __restrict__ data, size_t n_groups) {
+    const int lane = threadIdx.x & 31;
+    const size_t warps = (size_t)gridDim.x * (blockDim.x >> 5);
+    for (size_t g = (size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < n_groups; g += warps) {
+        uint4* p = reinterpret_cast<uint4*>(data + g * 512) + lane;
+        const uint4 v = __ldcs(p);
+        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        butterfly_rows<ELEM>(w, lane);
+        __stcs(p, make_uint4(w[0], w[1], w[2], w[3]));
+    }
+}
+
+// Image transpose, full 64x64 (u8) / 64x64 (u16) tiles: coalesced 128-bit loads into a padded
+// shared tile, 16-byte rows of 16x16 (u8) / 8x8 (u16) blocks into registers, register butterfly,
+// 128-bit stores of output rows (lane groups paired so every output row gets 32 / 64 contiguous
+// bytes per warp store).
+template <typename T>
+__global__ void __launch_bounds__(256)
+transpose_image_bfly_kernel(const T* __restrict__ src, size_t sp, T* __restrict__ dst, size_t dp, int W, int H) {
+    constexpr int ELEM = sizeof(T);
+    constexpr int TBY = 64;                      // tile rows
+    constexpr int RB = 256;                      // tile row bytes (256 u8 / 128 u16 columns)
+    constexpr int TBX = RB / ELEM;
+    constexpr int PB = RB + 16;                  // padded smem row pitch (bank-conflict free)
+    constexpr int BS = 16 / ELEM;                // block side (16 u8 / 8 u16)
+    constexpr int NBX = TBX / BS, NBY = TBY / BS;
+    __shared__ __align__(16) unsigned char tile[TBY * PB];
+    const int x0 = blockIdx.x * TBX, y0 = blockIdx.y * TBY;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned char* s8 = reinterpret_cast<const unsigned char*>(src);
+    unsigned char* d8 = reinterpret_cast<unsigned char*>(dst);
+    constexpr int CPR = RB / 16;                 // 16-byte chunks per tile row
+    constexpr int LPT = TBY * CPR / 256;         // loads per thread (4), all issued before the stores
+    uint4 v[LPT];
+#pragma unroll
+    for (int k = 0; k < LPT; ++k) {
+        const int c = tid + 256 * k, r = c / CPR, cc = c % CPR;
+        v[k] = __ldcs(reinterpret_cast<const uint4*>(s8 + (size_t)(y0 + r) * sp + (size_t)x0 * ELEM + cc * 16));
+    }
+#pragma unroll
+    for (int k = 0; k < LPT; ++k) {
+        const int c = tid + 256 * k, r = c / CPR, cc = c % CPR;
+        *reinterpret_cast<uint4*>(tile + r * PB + cc * 16) = v[k];
+    }
+    __syncthreads();
+    // blocks (b, c): b = block row (input rows), c = block column (input columns). A warp job is
+    // GPW consecutive b for one c; lane group g = lane / BS handles b = bq * GPW + g, so one
+    // output row receives GPW * 16 contiguous bytes per warp store.
+    constexpr int GPW = 32 / BS;
+    constexpr int JOBS = NBX * NBY / GPW;
+    const int i = lane % BS, g = lane / BS;
+#pragma unroll
+    for (int job = warp; job < JOBS; job += 8) {
+        const int c = job % NBX, bq = job / NBX;
+        const int b = bq * GPW + g;
+        const uint4 t = *reinterpret_cast<const uint4*>(tile + (b * BS + i) * PB + c * 16);
+        uint32_t w[4] = {t.x, t.y, t.z, t.w};
+        butterfly_rows<ELEM>(w, i);
+        // lane holds input column c*BS + i, rows b*BS .. b*BS+BS-1 = output row x0 + c*BS + i
+        __stcs(reinterpret_cast<uint4*>(d8 + (size_t)(x0 + c * BS + i) * dp + (size_t)(y0 + b * BS) * ELEM),
+               make_uint4(w[0], w[1], w[2], w[3]));
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // K5: batched tile transposes, one tile per thread (contiguous tiles)
 // ------------------------------------------------------------------------------------------
 // 4x4 byte transpose of four row words a[0..3] -> column words b[0..3].
@@ -163,14 +265,33 @@ tiles_generic_kernel(T* __restrict__ data, size_t n_tiles, int n, size_t row_str
 
 cudaError_t launch_transpose(const void* src, size_t sp, void* dst, size_t dp, int W, int H, int elem,
                              cudaStream_t s) {
-    dim3 grid(cdiv(W, kTT), cdiv(H, kTT));
     const int vec_ok = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | sp | dp) & 15) == 0;
-    if (elem == 1)
-        transpose_image_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)src, sp, (uint8_t*)dst, dp, W, H, vec_ok);
-    else
-        transpose_image_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)src, sp / 2, (uint16_t*)dst,
-                                                              dp / 2, W, H, vec_ok);
-    count_launch();
+    const int TX = 256 / elem;  // butterfly tile: 64 rows x 256 bytes
+    const int FW = vec_ok ? W / TX * TX : 0, FH = vec_ok ? H / kTT * kTT : 0;  // full-tile region
+    if (FW && FH) {
+        dim3 grid(FW / TX, FH / kTT);
+        if (elem == 1)
+            transpose_image_bfly_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)src, sp, (uint8_t*)dst, dp, W, H);
+        else
+            transpose_image_bfly_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)src, sp, (uint16_t*)dst, dp, W, H);
+        count_launch();
+    }
+    // ragged right columns / bottom rows (and unaligned images): the shared-memory tile kernel
+    auto ragged = [&](int xs, int ys, int w, int h) {
+        if (w <= 0 || h <= 0) return;
+        dim3 grid(cdiv(w, kTT), cdiv(h, kTT));
+        const char* sb = static_cast<const char*>(src) + (size_t)ys * sp + (size_t)xs * elem;
+        char* db = static_cast<char*>(dst) + (size_t)xs * dp + (size_t)ys * elem;
+        const int v = ((reinterpret_cast<uintptr_t>(sb) | reinterpret_cast<uintptr_t>(db) | sp | dp) & 15) == 0;
+        if (elem == 1)
+            transpose_image_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)sb, sp, (uint8_t*)db, dp, w, h, v);
+        else
+            transpose_image_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)sb, sp / 2, (uint16_t*)db, dp / 2, w, h,
+                                                                  v);
+        count_launch();
+    };
+    ragged(FW, 0, W - FW, H);   // right strip, all rows
+    ragged(0, FH, FW, H - FH);  // bottom strip under the full tiles
     return cudaGetLastError();
 }
 
@@ -180,6 +301,15 @@ cudaError_t launch_transpose_tiles(void* data, size_t n_tiles, int n, size_t row
     const bool contiguous = row_stride == (size_t)n && tile_step == (size_t)n * n &&
                             (reinterpret_cast<uintptr_t>(data) & 15) == 0;
     const unsigned blocks = (unsigned)((n_tiles + 127) / 128);
+    if (contiguous && ((elem == 1 && n == 16) || (elem == 2 && n == 8)) && n_tiles % (elem == 1 ? 2 : 4) == 0) {
+        const size_t groups = n_tiles * n * n * elem / 512;
+        const size_t want = (groups + 7) / 8;
+        const unsigned grid = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+        if (elem == 1) tiles_warp_kernel<1><<<grid, 256, 0, s>>>((uint8_t*)data, groups);
+        else tiles_warp_kernel<2><<<grid, 256, 0, s>>>((uint8_t*)data, groups);
+        count_launch();
+        return cudaGetLastError();
+    }
     if (contiguous && elem == 1) {
         if (n == 4) tiles_u8_kernel<4><<<blocks, 128, 0, s>>>((uint8_t*)data, n_tiles);
         else if (n == 8) tiles_u8_kernel<8><<<blocks, 128, 0, s>>>((uint8_t*)data, n_tiles);

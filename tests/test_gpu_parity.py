@@ -241,6 +241,23 @@ def test_transpose_images(gpu, restatement):
             assert np.array_equal(gpu.transpose_image(img), img.T)
 
 
+def test_transpose_images_aligned(gpu, restatement):
+    # 16-byte aligned pitches: full 64x64 tiles through the register-butterfly kernel, ragged
+    # right / bottom strips through the shared-memory kernel
+    import torch
+    for dtype in (np.uint8, np.uint16):
+        es = np.dtype(dtype).itemsize
+        for (h, w) in [(64, 64), (128, 192), (100, 333), (65, 1000), (1000, 65), (512, 2048), (777, 1500)]:
+            img = restatement.generate(w, h, 3 * h + w, dtype=dtype)
+            src = to_device(img, (-w) % (16 // es) + 16 // es)
+            dst = empty_device((w, h), dtype, (-h) % (16 // es), 0x3C)
+            gpu.transpose_device(src, dst)
+            torch.cuda.synchronize()
+            assert np.array_equal(to_host(dst), img.T), (dtype, h, w)
+            full = to_host_full(dst, h + (-h) % (16 // es))
+            assert np.all(full[:, h:] == 0x3C), ("padding written", dtype, h, w)
+
+
 def test_transpose_tiles(gpu, restatement):
     import torch
     for dt in (np.uint8, np.uint16, np.uint32):
