@@ -73,7 +73,7 @@ const char* plan_name(const MorphJob& j) {
     int R = 0;
     if (!choose(k, &R)) return nullptr;
     snprintf(buf, sizeof(buf), "col_%s_w%dx%d_R%d_smem%dK", j.elem == 1 ? "u8" : "u16", 2 * j.gx + 1, 2 * j.gy + 1, R,
-             SMEM / 1024);
+             (j.gx == 0 ? ColGeo<0>::SMEM : ColGeo<1>::SMEM) / 1024);
     return buf;
 }
 

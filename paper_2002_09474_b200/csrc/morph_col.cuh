@@ -29,14 +29,22 @@ using stream::tma_box;
 constexpr int WPB = RM_COL_WPB;      // warps per CTA (independent pipelines sharing one smem block)
 constexpr int BR = RM_COL_BR;        // rows per TMA block
 constexpr int NS = RM_COL_NS;        // ring slots per warp
-constexpr int HALO = 16;             // halo bytes left / right of a strip row
 constexpr int SB = 512;              // strip bytes per row (32 lanes x 16 B)
-constexpr int RB = SB + 2 * HALO;    // bytes per staged row (544)
-constexpr int SLOTB = BR * RB;       // 4352 = 34 x 128 (TMA destinations stay 128-B aligned)
-constexpr int WARPB = NS * SLOTB;
 constexpr int HDR = 128;             // mbarriers
-constexpr int SMEM = HDR + WPB * WARPB;
-constexpr int GMAX = 3;
+// Slot layout: the 8 staged rows' 512 strip bytes (dense, one 512-byte-aligned TMA box) and, when
+// the horizontal window needs neighbours, the 16 bytes left / right of the strip for each row in
+// two small regions (two 16-byte-wide TMA boxes), so the big box stays aligned to whole 128-byte
+// lines. Slot = 4096 (+ 2 x 128) bytes, a multiple of 128.
+template <int GX>
+struct ColGeo {
+    static constexpr int HALO = GX == 0 ? 0 : 16;
+    static constexpr int MAINB = BR * SB;
+    static constexpr int LEFT = MAINB, RIGHT = MAINB + BR * 16;
+    static constexpr int SLOTB = MAINB + (HALO ? 2 * BR * 16 : 0);
+    static constexpr int WARPB = NS * SLOTB;
+    static constexpr int SMEM = HDR + WPB * WARPB;
+};
+constexpr int GMAX = 3;  // largest wing handled here (windows up to 7 x 7)
 
 struct ColParams {
     const uint8_t* src;  // output row 0 of image 0
@@ -162,11 +170,13 @@ struct ColCore {
     static constexpr int PXL = 16 / sz;  // pixels per lane
 
     // load one staged row into expanded words
-    static __device__ __forceinline__ void load_row(const unsigned char* row, int lane, uint32_t* e) {
-        const uint4 m = *reinterpret_cast<const uint4*>(row + HALO + lane * 16);
+    using CG = ColGeo<GX>;
+    static __device__ __forceinline__ void load_row(const unsigned char* slot, int r, int lane, uint32_t* e) {
+        const uint4 m = *reinterpret_cast<const uint4*>(slot + r * SB + lane * 16);
         const uint32_t w[4] = {m.x, m.y, m.z, m.w};
-        const int xo = lane == 0 ? HALO - 8 : HALO + SB;
-        const uint2 xx = *reinterpret_cast<const uint2*>(row + xo);
+        uint2 xx = make_uint2(0, 0);  // halo words (lane 0: left of the strip, lane 31: right)
+        if constexpr (GX > 0)
+            xx = *reinterpret_cast<const uint2*>(slot + (lane == 0 ? CG::LEFT + 8 : CG::RIGHT) + r * 16);
         if constexpr (sz == 1) {
             const uint32_t x = lane == 0 ? xx.y : xx.x;  // left: bytes x0-4..x0-1; right: x0+512..
 #pragma unroll
@@ -274,28 +284,33 @@ static __device__ __noinline__ void store_partial(uint8_t* d, uint4 out, int nby
 // Border strips: overwrite the staged out-of-image columns of one block in shared memory
 // (replicate: the row's first / last pixel; constant: the border value), so the row loop itself
 // has no border logic. Lane-parallel, border strips only.
-template <typename T>
-__device__ __forceinline__ void fix_block_columns(unsigned char* blk, int lane, int x0, int W, int cmode, uint32_t bv) {
+template <typename T, int GX>
+__device__ __forceinline__ unsigned char* staged_byte(unsigned char* slot, int r, int m) {
+    using CG = ColGeo<GX>;
+    return m < 0 ? slot + CG::LEFT + r * 16 + (m + 16)
+                 : (m < SB ? slot + r * SB + m : slot + CG::RIGHT + r * 16 + (m - SB));
+}
+template <typename T, int GX>
+__device__ __forceinline__ void fix_block_columns(unsigned char* slot, int lane, int x0, int W, int cmode, uint32_t bv) {
     constexpr int sz = sizeof(T);
-    if (x0 == 0) {  // 16 halo bytes left of column 0: 8 rows x 4 words = one word per lane
+    constexpr int HALO = ColGeo<GX>::HALO;
+    if (HALO > 0 && x0 == 0) {  // 16 halo bytes left of column 0: 8 rows x 4 words = one word per lane
         const int r = lane >> 2, wI = lane & 3;
-        unsigned char* row = blk + r * RB;
         uint32_t f = bv;
-        if (cmode == 0) f = sz == 1 ? row[HALO] * 0x01010101u : *reinterpret_cast<const uint16_t*>(row + HALO) * 0x00010001u;
+        if (cmode == 0)
+            f = sz == 1 ? slot[r * SB] * 0x01010101u : *reinterpret_cast<const uint16_t*>(slot + r * SB) * 0x00010001u;
         __syncwarp();
-        reinterpret_cast<uint32_t*>(row)[wI] = f;
+        reinterpret_cast<uint32_t*>(slot + ColGeo<GX>::LEFT + r * 16)[wI] = f;
     }
-    const int start = HALO + (W - x0) * sz;  // first staged byte at column >= W
-    if (start < RB) {
-        const int wstart = (start + 3) >> 2;    // first whole word
+    const int start = (W - x0) * sz;  // first staged byte (from the strip start) at column >= W
+    if (start < SB + HALO) {
         for (int r = 0; r < BR; ++r) {
-            unsigned char* row = blk + r * RB;
             uint32_t f = bv;
             if (cmode == 0)
-                f = sz == 1 ? row[start - 1] * 0x01010101u : *reinterpret_cast<const uint16_t*>(row + start - 2) * 0x00010001u;
+                f = sz == 1 ? *staged_byte<T, GX>(slot, r, start - 1) * 0x01010101u
+                            : *reinterpret_cast<const uint16_t*>(staged_byte<T, GX>(slot, r, start - 2)) * 0x00010001u;
             __syncwarp();
-            for (int i = start + lane; i < min(wstart * 4, RB); i += 32) row[i] = (uint8_t)(f >> (8 * (i & 3)));
-            for (int wI = wstart + lane; wI < RB / 4; wI += 32) reinterpret_cast<uint32_t*>(row)[wI] = f;
+            for (int m = start + lane; m < SB + HALO; m += 32) *staged_byte<T, GX>(slot, r, m) = (uint8_t)(f >> (8 * (m & 3)));
         }
     }
     __syncwarp();
@@ -303,7 +318,7 @@ __device__ __forceinline__ void fix_block_columns(unsigned char* blk, int lane, 
 
 template <typename T, int MODE, int GX, int GY>
 __global__ void __launch_bounds__(WPB * 32)
-morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap) {
+morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap hmap) {
     constexpr int sz = sizeof(T);
     constexpr int PXL = 16 / sz;
     constexpr int SWPX = SB / sz;
@@ -311,6 +326,8 @@ morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int RING = WV == 1 ? 1 : (WV <= 4 ? 4 : 8);  // power of two dividing BR: compile-time slots
     constexpr int NW = RowW<T>::N;
     using C = ColCore<T, MODE, GX, GY>;
+    using CG = ColGeo<GX>;
+    constexpr int HALO = CG::HALO, SLOTB = CG::SLOTB, WARPB = CG::WARPB;
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -339,36 +356,43 @@ morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap) {
         unsigned char* dstb = ring + islot * SLOTB;
         uint64_t* bar = &bars[islot];
         const int yb = iit.y0 - GY + ib * BR;
-        const int xb = iit.x0 * sz - HALO;  // byte column of the staged row start
+        const int xb = iit.x0 * sz;  // byte column of the strip start
         if (p.use_tma && yb >= p.row_lo && yb + BR <= p.row_hi) {
             if (lane == 0) {
                 mbar_arrive_tx(bar, (uint32_t)SLOTB);
                 tma_box(dstb, &tmap, xb / 4, yb - p.row_lo, iit.b, bar);
+                if constexpr (HALO > 0) {
+                    tma_box(dstb + CG::LEFT, &hmap, (xb - 16) / 4, yb - p.row_lo, iit.b, bar);
+                    tma_box(dstb + CG::RIGHT, &hmap, (xb + SB) / 4, yb - p.row_lo, iit.b, bar);
+                }
             }
         } else {
-            // border block: one bulk copy per row (clamped row / constant fill), clipped columns
+            // border block: bulk copies per row (clamped row / constant fill), clipped columns
             const int y = yb + lane;
             const bool inrow = lane < BR;
             const bool outside = p.cmode && (y < p.row_lo || y >= p.row_hi);
-            const int c0 = max(xb, 0);
-            const int c1 = min(xb + RB, (int)p.sp);
-            const int len = c1 - c0;
-            const unsigned cp = __ballot_sync(0xffffffffu, inrow && !outside);
+            const int len = min(SB, (int)p.sp - xb);
+            const bool lft = HALO > 0 && xb >= 16, rgt = HALO > 0 && xb + SB + 16 <= (int)p.sp;
+            const bool cp = inrow && !outside;
+            const int bytes = __reduce_add_sync(0xffffffffu, cp ? len + (lft ? 16 : 0) + (rgt ? 16 : 0) : 0);
             unsigned fillm = __ballot_sync(0xffffffffu, inrow && outside);
             while (fillm) {
                 const int r = __ffs(fillm) - 1;
                 fillm &= fillm - 1;
-                for (int c = lane; c < RB / 16; c += 32)
-                    reinterpret_cast<uint4*>(dstb + r * RB)[c] = make_uint4(bv, bv, bv, bv);
+                reinterpret_cast<uint4*>(dstb + r * SB)[lane] = make_uint4(bv, bv, bv, bv);
+                if (HALO > 0 && lane < 2)
+                    *reinterpret_cast<uint4*>(dstb + (lane ? CG::RIGHT : CG::LEFT) + r * 16) = make_uint4(bv, bv, bv, bv);
             }
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive_tx(bar, (uint32_t)(__popc(cp) * len));
+            if (lane == 0) mbar_arrive_tx(bar, (uint32_t)bytes);
             __syncwarp();
-            if (inrow && !outside) {
+            if (cp) {
                 const int yc = min(max(y, p.row_lo), p.row_hi - 1);
-                bulk_g2s(dstb + lane * RB + (c0 - xb),
-                         p.src + (size_t)iit.b * p.simg + (ptrdiff_t)yc * (ptrdiff_t)p.sp + c0, (uint32_t)len, bar);
+                const uint8_t* srow = p.src + (size_t)iit.b * p.simg + (ptrdiff_t)yc * (ptrdiff_t)p.sp;
+                bulk_g2s(dstb + lane * SB, srow + xb, (uint32_t)len, bar);
+                if (lft) bulk_g2s(dstb + CG::LEFT + lane * 16, srow + xb - 16, 16u, bar);
+                if (rgt) bulk_g2s(dstb + CG::RIGHT + lane * 16, srow + xb + SB, 16u, bar);
             }
         }
         islot = islot + 1 == NS ? 0 : islot + 1;
@@ -398,13 +422,13 @@ morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap) {
         for (int blk = 0; blk < it.nblk; ++blk) {
             mbar_wait(&bars[cslot], cpar);
             const unsigned char* rows = ring + cslot * SLOTB;
-            if (edge) fix_block_columns<T>(ring + cslot * SLOTB, lane, it.x0, p.W, p.cmode, bv);
+            if (edge) fix_block_columns<T, GX>(ring + cslot * SLOTB, lane, it.x0, p.W, p.cmode, bv);
             // 8 rows; the row-validity test only in blocks with warm-up rows or rows past the band
             auto block = [&](auto check_tag) {
                 constexpr bool CHECK = decltype(check_tag)::value;
 #pragma unroll
                 for (int r = 0; r < BR; ++r) {
-                    C::load_row(rows + r * RB, lane, E[r % RING]);
+                    C::load_row(rows, r, lane, E[r % RING]);
                     if (!CHECK || (unsigned)(o + r) < (unsigned)it.rows_out) {
                         uint32_t v[NW];
 #pragma unroll
@@ -455,7 +479,12 @@ cudaError_t launch_col_variant(const MorphJob& j, int R) {
     p.nstrips = cdiv(j.W * (int)sizeof(T), SB);
     p.nbands = cdiv(j.H, R);
     CUtensorMap map;
-    p.use_tma = stream::encode_input_map(j, RB / 4, BR, &map) ? 1 : 0;
+    using CG = ColGeo<GX>;
+    constexpr int SMEM = CG::SMEM;
+    CUtensorMap hmap;
+    p.use_tma = stream::encode_input_map(j, SB / 4, BR, &map) ? 1 : 0;
+    if (p.use_tma && CG::HALO > 0) p.use_tma = stream::encode_input_map(j, 4, BR, &hmap) ? 1 : 0;
+    else memset(&hmap, 0, sizeof(hmap));
     auto kern = morph_col_kernel<T, MODE, GX, GY>;
     cudaError_t e = cudaSuccess;
     const int occ = kernel_occupancy((const void*)kern, WPB * 32, SMEM, &e);
@@ -474,7 +503,7 @@ cudaError_t launch_col_variant(const MorphJob& j, int R) {
     p.strip_s = fs.s;
     p.img_m = fi.m;
     p.img_s = fi.s;
-    kern<<<dim3((unsigned)ctas), WPB * 32, SMEM, j.stream>>>(p, map);
+    kern<<<dim3((unsigned)ctas), WPB * 32, SMEM, j.stream>>>(p, map, hmap);
     count_launch();
     return cudaGetLastError();
 }
