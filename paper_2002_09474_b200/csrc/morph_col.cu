@@ -46,6 +46,10 @@ bool choose(const MorphJob& j, int* R) {
     const long warps = 148L * 16;
     const long rows_per_warp = std::max(1L, ((long)j.H * strips + warps - 1) / warps);
     int m = (int)std::max(2L, std::min(16L, (rows_per_warp + 2 * j.gy + BR - 1) / BR));
+    // small images: with two-block items fewer than half the resident warps would get work, so
+    // use single-block items (more warps in flight beats the extra halo rows)
+    if (m == 2 && BR - 2 * j.gy >= 4 && (long)((j.H + (2 * BR - 2 * j.gy) - 1) / (2 * BR - 2 * j.gy)) * strips < warps / 2)
+        m = 1;
     if (const char* e = getenv("RMGPU_COL_BLOCKS")) m = std::max(1, atoi(e));
     int r = m * BR - 2 * j.gy;
     if (r < 1) r = BR;
