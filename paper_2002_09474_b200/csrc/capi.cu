@@ -171,20 +171,32 @@ int check_op_border(int op, int border, unsigned bval, int elem) {
     return RMGPU_OK;
 }
 
-// Scratch images (compound ops, two-pass fallback) come from the device's default stream-ordered
-// pool; keep freed blocks cached so repeated calls do not return memory to the driver.
-void keep_pool_cached() {
-    static std::atomic<unsigned long long> done{0};
+// Scratch buffers (compound-op intermediates, two-pass fallback, host-entry staging) come from a
+// private stream-ordered pool per device that keeps freed blocks cached between calls, so repeated
+// calls never go back to the driver and the application's default pool is left untouched.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
-    const unsigned long long bit = 1ull << dev;
-    if (done.load(std::memory_order_relaxed) & bit) return;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (!pools[dev]) {
+            cudaMemPoolProps props = {};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            e = cudaMemPoolCreate(&pools[dev], &props);
+            if (e != cudaSuccess) return e;
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool = pools[dev];
     }
-    done.fetch_or(bit, std::memory_order_relaxed);
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
 // One erode / dilate / gradient over the job's rows. Window-1 axes are a copy
@@ -228,8 +240,7 @@ int run_single(MorphJob j) {
     const size_t tmp_img = tmp_pitch * (size_t)j.H;
     const int nbuf = j.mode == rmgpu::MODE_GRAD ? 3 : 1;
     void* tmp = nullptr;
-    keep_pool_cached();
-    RM_CUDA(cudaMallocAsync(&tmp, tmp_img * j.batch * nbuf, j.stream));
+    RM_CUDA(scratch_alloc(&tmp, tmp_img * j.batch * nbuf, j.stream));
     auto run_pair = [&](int mode, void* out, size_t out_pitch, size_t out_img) -> int {
         MorphJob v = j;
         v.mode = mode;
@@ -305,8 +316,7 @@ int run_morph(const void* src, size_t sp, size_t simg, void* dst, size_t dp, siz
     const size_t tp = (row_bytes + 255) & ~size_t(255);
     const size_t timg = tp * (size_t)IH;
     void* tmp = nullptr;
-    keep_pool_cached();
-    RM_CUDA(cudaMallocAsync(&tmp, timg * batch, stream));
+    RM_CUDA(scratch_alloc(&tmp, timg * batch, stream));
     MorphJob a = j;
     a.mode = op == RMGPU_OPEN ? rmgpu::MODE_MIN : rmgpu::MODE_MAX;
     a.src = static_cast<const char*>(src) - (ptrdiff_t)ia * (ptrdiff_t)sp;
@@ -345,11 +355,6 @@ int host_stream(cudaStream_t* out) {
     if (t_ctx.stream == nullptr || t_ctx.device != dev) {
         RM_CUDA(cudaStreamCreateWithFlags(&t_ctx.stream, cudaStreamNonBlocking));
         t_ctx.device = dev;
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;  // keep freed blocks cached between calls
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
     }
     *out = t_ctx.stream;
     return RMGPU_OK;
@@ -373,8 +378,8 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     const size_t rb = (size_t)W * elem, pitch = (rb + 255) & ~size_t(255);
     DevBuf a, b;
     a.s = b.s = s;
-    RM_CUDA(cudaMallocAsync(&a.p, pitch * H, s));
-    RM_CUDA(cudaMallocAsync(&b.p, pitch * H, s));
+    RM_CUDA(scratch_alloc(&a.p, pitch * H, s));
+    RM_CUDA(scratch_alloc(&b.p, pitch * H, s));
     RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, rb, H, cudaMemcpyHostToDevice, s));
     rc = run_morph(a.p, pitch, 0, b.p, pitch, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, elem, s);
     if (rc) return rc;
@@ -496,7 +501,7 @@ int rmgpu_window_1d_u8(const void* in, size_t n, int window, int op, int border,
                          (cudaStream_t)stream);
     cudaStream_t s = (cudaStream_t)stream;
     void* tmp = nullptr;
-    RM_CUDA(cudaMallocAsync(&tmp, n, s));
+    RM_CUDA(scratch_alloc(&tmp, n, s));
     RM_CUDA(cudaMemcpyAsync(tmp, in, n, cudaMemcpyDeviceToDevice, s));
     rc = pass_impl(RMGPU_PASS_HORIZONTAL, tmp, n, out, n, (int)n, 1, window, op, border, bval, s);
     cudaFreeAsync(tmp, s);
@@ -549,8 +554,8 @@ static int transpose_host(const void* hsrc, size_t sp, void* hdst, size_t dp, in
     const size_t pa = ((size_t)W * elem + 255) & ~size_t(255), pb = ((size_t)H * elem + 255) & ~size_t(255);
     DevBuf a, b;
     a.s = b.s = s;
-    RM_CUDA(cudaMallocAsync(&a.p, pa * H, s));
-    RM_CUDA(cudaMallocAsync(&b.p, pb * W, s));
+    RM_CUDA(scratch_alloc(&a.p, pa * H, s));
+    RM_CUDA(scratch_alloc(&b.p, pb * W, s));
     RM_CUDA(cudaMemcpy2DAsync(a.p, pa, hsrc, sp, (size_t)W * elem, H, cudaMemcpyHostToDevice, s));
     cudaError_t e = rmgpu::launch_transpose(a.p, pa, b.p, pb, W, H, elem, s);
     if (e != cudaSuccess) return cuda_fail(e, "transpose");
@@ -578,7 +583,7 @@ int rmgpu_transpose_tiles_host(void* hdata, int elem, size_t n_tiles, int n, siz
     const size_t span = ((n_tiles - 1) * step + (size_t)(n - 1) * rs + n) * elem;
     DevBuf a;
     a.s = s;
-    RM_CUDA(cudaMallocAsync(&a.p, span, s));
+    RM_CUDA(scratch_alloc(&a.p, span, s));
     RM_CUDA(cudaMemcpyAsync(a.p, hdata, span, cudaMemcpyHostToDevice, s));
     if ((rc = tiles_impl(a.p, n_tiles, n, rs, step, elem, s))) return rc;
     RM_CUDA(cudaMemcpyAsync(hdata, a.p, span, cudaMemcpyDeviceToHost, s));
@@ -598,8 +603,8 @@ int rmgpu_pass_host_u8(int which, const void* hsrc, size_t sp, void* hdst, size_
     const size_t pitch = ((size_t)W + 255) & ~size_t(255);
     DevBuf a, b;
     a.s = b.s = s;
-    RM_CUDA(cudaMallocAsync(&a.p, pitch * H, s));
-    RM_CUDA(cudaMallocAsync(&b.p, pitch * H, s));
+    RM_CUDA(scratch_alloc(&a.p, pitch * H, s));
+    RM_CUDA(scratch_alloc(&b.p, pitch * H, s));
     RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, W, H, cudaMemcpyHostToDevice, s));
     if ((rc = pass_impl(which, a.p, pitch, b.p, pitch, W, H, window, op, border, bval, s))) return rc;
     RM_CUDA(cudaMemcpy2DAsync(hdst, dp, b.p, pitch, W, H, cudaMemcpyDeviceToHost, s));
