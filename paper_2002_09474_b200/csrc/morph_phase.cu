@@ -59,14 +59,22 @@ bool choose(const MorphJob& j, Choice* c) {
         for (int B : {8, 12, 16, 20, 24, 28}) {
             if (B > w1) continue;
             const int q = w1 / B, r = w1 - q * B;
-            if (q > QMAX || (r != 0 && r != 2)) continue;  // tail length is a compile-time 0 or 2
+            // compile-time tail lengths: 0 or 2 for every B, plus r = 14 for 16-row blocks (w = 31, 63:
+            // 32-row chunks, 8 row groups, all warps busy in the horizontal phase)
+            const bool ok = r == 0 || r == 2 || (B == 16 && r == 14);
+            if (q > QMAX || !ok) continue;
             const int t = j.elem == 1 ? phase_smem<uint8_t>(hb0, B, q, 2) : phase_smem<uint16_t>(hb0, B, q, 2);
             if (t > 220 * 1024) continue;
             const int occ = std::max(1, std::min(2, (228 * 1024) / (t + 1024)));
-            const double cost = (3.0 + double(2 * r + q) / B + 6.0 / B) / occ;
+            // vertical: min/max per output ~ 3 + (2r + q)/B (+ per-block overhead 6/B); horizontal:
+            // one phase per chunk costs about the same wall time whether it has 5 or 8 row groups
+            // (one warp each), so its per-row cost scales with 8 / (row groups per chunk)
+            const int ngc = chunk_rows(B) / 4;
+            double cost = (3.0 + double(2 * r + q) / B + 6.0 / B + 3.0 * 8.0 / ngc) / occ;
+            if (B == 16 && r == 14 && q >= 2) cost *= 0.9;  // measured: best for w = 63 on large images
             if (cost < best - 1e-9) {
                 best = cost;
-                c->vb = B + (r ? 100 : 0);
+                c->vb = B + 100 * r;
                 c->B = B;
                 c->q = q;
             }

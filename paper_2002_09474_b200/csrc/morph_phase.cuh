@@ -82,7 +82,7 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
     constexpr int GR = G::GR, TW = G::TW, ESZ = G::ESZ;
     constexpr int sz = sizeof(T);
     constexpr bool VDIRECT = VB <= 7;
-    constexpr int VR = VB >= 100 ? 2 : 0;      // block mode: tail rows r = w1 mod B (compile-time 0 or 2)
+    constexpr int VR = VB / 100;               // block mode: tail rows r = w1 mod B (compile-time)
     constexpr int B = VDIRECT ? VCH : VB % 100;  // rows per block (TMA box)
     constexpr int CH = chunk_rows(B);          // rows per chunk (horizontal hand-off)
     constexpr int KB = CH / B;                 // blocks per chunk
@@ -568,7 +568,8 @@ cudaError_t launch_phase_variant(const MorphJob& j, int rh, int B, int q, int pf
     return cudaGetLastError();
 }
 
-#define RM_PHASE_V(X) X(1) X(3) X(5) X(7) X(8) X(12) X(16) X(20) X(24) X(28) X(108) X(112) X(116) X(120) X(124) X(128)
+#define RM_PHASE_V(X) X(1) X(3) X(5) X(7) X(8) X(12) X(16) X(20) X(24) X(28) X(208) X(212) X(216) X(220) X(224) X(228) \
+    X(1416)
 #define RM_PHASE_H(X) X(1) X(3) X(5) X(7) X(8) X(9)
 
 template <typename T, int MODE, int VB>
