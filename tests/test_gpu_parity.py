@@ -258,6 +258,23 @@ def test_transpose_images_aligned(gpu, restatement):
             assert np.all(full[:, h:] == 0x3C), ("padding written", dtype, h, w)
 
 
+def test_host_entry_pipelined_bands(gpu, restatement):
+    # host-buffer entry point on images large enough to be pipelined in row bands (H2D / kernel /
+    # D2H overlapped): identical to the device-buffer call on the whole image
+    import torch
+    for dtype, (w, h) in ((np.uint8, (4096, 2048)), (np.uint16, (1500, 1999))):
+        img = restatement.generate(w, h, 77, dtype=dtype)
+        mx = int(np.iinfo(dtype).max)
+        for (wx, wy, op, border, bval) in [(3, 3, ERODE, REPLICATE, 0), (63, 63, DILATE, REPLICATE, 0),
+                                           (21, 21, OPEN, CONSTANT, mx // 3), (5, 31, CLOSE, REPLICATE, 0),
+                                           (7, 7, GRADIENT, CONSTANT, 9), (1, 101, ERODE, CONSTANT, mx)]:
+            fn = {ERODE: gpu.erode, DILATE: gpu.dilate, OPEN: gpu.opening, CLOSE: gpu.closing,
+                  GRADIENT: gpu.gradient}[op]
+            got = fn(img, gpu.StructuringElement(wx, wy), gpu.BorderPolicy(border, bval))
+            want, _ = gpu_morph(gpu, img, wx, wy, op, border, bval)
+            assert np.array_equal(got, want), (dtype, wx, wy, op, border)
+
+
 def test_transpose_tiles(gpu, restatement):
     import torch
     for dt in (np.uint8, np.uint16, np.uint32):
