@@ -32,7 +32,7 @@ CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_fast.cu", "morph_fast_u8_min
               "morph_stream_u8_max.cu", "morph_stream_u16_min.cu", "morph_stream_u16_max.cu", "morph_phase.cu",
               "morph_phase_u8_min.cu", "morph_phase_u8_max.cu", "morph_phase_u16_min.cu", "morph_phase_u16_max.cu",
               "morph_col.cu", "morph_col_u8_min.cu", "morph_col_u8_max.cu", "morph_col_u16_min.cu",
-              "morph_col_u16_max.cu", "transpose.cu",
+              "morph_col_u16_max.cu", "morph_col_u8_grad.cu", "morph_col_u16_grad.cu", "transpose.cu",
               "generate.cu"]
 HOST_SOURCES = [os.path.join("host", "rectmorph_b200.cpp")]
 

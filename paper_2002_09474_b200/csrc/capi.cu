@@ -221,6 +221,34 @@ int run_single(MorphJob j) {
         if (e != cudaSuccess) return cuda_fail(e, "phase morph kernel");
         return RMGPU_OK;
     }
+    if (j.mode == rmgpu::MODE_GRAD && !g_disable_stream && !g_prefer_stream) {
+        // large-window gradient: dilation into scratch and erosion into dst with the phase kernel,
+        // then dst = dilation - erosion (dispatch.cpp:58-71; never negative, no wrap)
+        const size_t rb = (size_t)j.W * j.elem, tp = (rb + 255) & ~size_t(255), timg = tp * (size_t)j.H;
+        void* hi = nullptr;
+        RM_CUDA(scratch_alloc(&hi, timg * j.batch, j.stream));
+        MorphJob mx = j;
+        mx.mode = rmgpu::MODE_MAX;
+        mx.dst = hi; mx.dp = tp; mx.dimg = timg;
+        int rc = RMGPU_OK;
+        if (rmgpu::phase::launch(mx, &e)) {
+            if (e != cudaSuccess) rc = cuda_fail(e, "phase morph kernel (gradient, dilation)");
+            MorphJob mn = j;
+            mn.mode = rmgpu::MODE_MIN;
+            if (rc == RMGPU_OK && (!rmgpu::phase::launch(mn, &e) || e != cudaSuccess))
+                rc = cuda_fail(e != cudaSuccess ? e : cudaErrorInvalidValue, "phase morph kernel (gradient, erosion)");
+            for (int b = 0; rc == RMGPU_OK && b < j.batch; ++b) {
+                char* d = static_cast<char*>(j.dst) + b * j.dimg;
+                e = rmgpu::launch_subtract(static_cast<char*>(hi) + b * timg, tp, d, j.dp, d, j.dp, j.W, j.H, j.elem,
+                                           j.stream);
+                if (e != cudaSuccess) rc = cuda_fail(e, "subtract");
+            }
+            cudaError_t fe = cudaFreeAsync(hi, j.stream);
+            if (rc == RMGPU_OK && fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
+            return rc;
+        }
+        cudaFreeAsync(hi, j.stream);
+    }
     if (!g_disable_stream && rmgpu::stream::launch(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "stream morph kernel");
         return RMGPU_OK;
@@ -448,6 +476,15 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
         if (const char* n = rmgpu::col::plan_name(j)) return n;
     if (!g_disable_stream && !g_prefer_stream)
         if (const char* n = rmgpu::phase::plan_name(j)) return n;
+    if (j.mode == rmgpu::MODE_GRAD && !g_disable_stream && !g_prefer_stream) {
+        MorphJob m = j;
+        m.mode = rmgpu::MODE_MAX;
+        if (const char* n = rmgpu::phase::plan_name(m)) {
+            static thread_local std::string g;
+            g = std::string("gradient[2x ") + n + " + subtract]";
+            return g.c_str();
+        }
+    }
     if (!g_disable_stream)
         if (const char* n = rmgpu::stream::plan_name(j)) return n;
     if (const char* n = rmgpu::fast_plan_name(j)) return n;

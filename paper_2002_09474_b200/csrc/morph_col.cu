@@ -29,11 +29,13 @@ cudaError_t dispatch_u8_min(const MorphJob&, int);
 cudaError_t dispatch_u8_max(const MorphJob&, int);
 cudaError_t dispatch_u16_min(const MorphJob&, int);
 cudaError_t dispatch_u16_max(const MorphJob&, int);
+cudaError_t dispatch_u8_grad(const MorphJob&, int);
+cudaError_t dispatch_u16_grad(const MorphJob&, int);
 
 namespace {
 
 bool choose(const MorphJob& j, int* R) {
-    if (j.mode != MODE_MIN && j.mode != MODE_MAX) return false;
+    if (j.mode != MODE_MIN && j.mode != MODE_MAX && j.mode != MODE_GRAD) return false;
     if (j.elem != 1 && j.elem != 2) return false;
     if (j.gx > GMAX || j.gy > GMAX) return false;
     if (getenv("RMGPU_NO_COL")) return false;
@@ -62,8 +64,11 @@ bool choose(const MorphJob& j, int* R) {
 bool launch(const MorphJob& j, cudaError_t* err) {
     int R = 0;
     if (!choose(j, &R)) return false;
-    if (j.elem == 1) *err = j.mode == MODE_MIN ? dispatch_u8_min(j, R) : dispatch_u8_max(j, R);
-    else *err = j.mode == MODE_MIN ? dispatch_u16_min(j, R) : dispatch_u16_max(j, R);
+    if (j.elem == 1)
+        *err = j.mode == MODE_MIN ? dispatch_u8_min(j, R) : j.mode == MODE_MAX ? dispatch_u8_max(j, R) : dispatch_u8_grad(j, R);
+    else
+        *err = j.mode == MODE_MIN ? dispatch_u16_min(j, R)
+                                  : j.mode == MODE_MAX ? dispatch_u16_max(j, R) : dispatch_u16_grad(j, R);
     return true;
 }
 

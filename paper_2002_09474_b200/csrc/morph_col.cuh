@@ -430,15 +430,34 @@ morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap, co
                 for (int r = 0; r < BR; ++r) {
                     C::load_row(rows, r, lane, E[r % RING]);
                     if (!CHECK || (unsigned)(o + r) < (unsigned)it.rows_out) {
-                        uint32_t v[NW];
+                        uint4 out;
+                        if constexpr (MODE == MODE_GRAD) {
+                            // morphological gradient from one read: dilation - erosion. Bytes (u8) /
+                            // halves (u16) of max are >= those of min, so one 32-bit subtract per
+                            // word never borrows across pixels.
+                            uint32_t vmin[NW], vmax[NW];
 #pragma unroll
-                        for (int w = 0; w < NW; ++w) {
-                            uint32_t col[WV];
+                            for (int w = 0; w < NW; ++w) {
+                                uint32_t col[WV];
 #pragma unroll
-                            for (int k = 0; k < WV; ++k) col[k] = E[(r - k + 8 * RING) % RING][w];
-                            v[w] = opn<MODE, WV>(col);
+                                for (int k = 0; k < WV; ++k) col[k] = E[(r - k + 8 * RING) % RING][w];
+                                vmin[w] = opn<MODE_MIN, WV>(col);
+                                vmax[w] = opn<MODE_MAX, WV>(col);
+                            }
+                            const uint4 lo = ColCore<T, MODE_MIN, GX, GY>::horizontal(vmin, lane);
+                            const uint4 hi = ColCore<T, MODE_MAX, GX, GY>::horizontal(vmax, lane);
+                            out = make_uint4(hi.x - lo.x, hi.y - lo.y, hi.z - lo.z, hi.w - lo.w);
+                        } else {
+                            uint32_t v[NW];
+#pragma unroll
+                            for (int w = 0; w < NW; ++w) {
+                                uint32_t col[WV];
+#pragma unroll
+                                for (int k = 0; k < WV; ++k) col[k] = E[(r - k + 8 * RING) % RING][w];
+                                v[w] = opn<MODE, WV>(col);
+                            }
+                            out = C::horizontal(v, lane);
                         }
-                        const uint4 out = C::horizontal(v, lane);
                         if (store_bytes == 16) *reinterpret_cast<uint4*>(drow) = out;
                         else store_partial(drow, out, store_bytes);
                     }

@@ -150,12 +150,23 @@ cudaError_t launch_pass_t(const MorphJob& j) {
 }
 
 template <typename T>
-__global__ void subtract_kernel(const T* __restrict__ a, size_t ap, const T* __restrict__ b, size_t bp,
-                                T* __restrict__ d, size_t dp, int W, int H) {
+__global__ void subtract_kernel(const T* __restrict__ a, size_t ap, const T* b, size_t bp, T* d, size_t dp,
+                                int W, int H) {  // b may alias d (in-place gradient)
     const int x = blockIdx.x * 64 + (threadIdx.x & 63);
     const int y = blockIdx.y * 4 + (threadIdx.x >> 6);
     if (x >= W || y >= H) return;
     d[(ptrdiff_t)y * dp + x] = (T)(a[(ptrdiff_t)y * ap + x] - b[(ptrdiff_t)y * bp + x]);
+}
+
+// a - b for 16-byte vectors of u8 or u16 pixels where every pixel of a is >= the one of b.
+__global__ void subtract16_kernel(const uint8_t* __restrict__ a, size_t ap, const uint8_t* b, size_t bp, uint8_t* d,
+                                  size_t dp, int vpr, int H) {
+    const int v = blockIdx.x * 64 + (threadIdx.x & 63);
+    const int y = blockIdx.y * 4 + (threadIdx.x >> 6);
+    if (v >= vpr || y >= H) return;
+    const uint4 x = *reinterpret_cast<const uint4*>(a + (size_t)y * ap + (size_t)v * 16);
+    const uint4 z = *reinterpret_cast<const uint4*>(b + (size_t)y * bp + (size_t)v * 16);
+    *reinterpret_cast<uint4*>(d + (size_t)y * dp + (size_t)v * 16) = make_uint4(x.x - z.x, x.y - z.y, x.z - z.z, x.w - z.w);
 }
 
 }  // namespace
@@ -188,13 +199,22 @@ cudaError_t launch_pass_cols(const MorphJob& j) {
 
 cudaError_t launch_subtract(const void* a, size_t ap, const void* b, size_t bp, void* dst, size_t dp,
                             int W, int H, int elem, cudaStream_t s) {
-    dim3 grid(cdiv(W, 64), cdiv(H, 4));
-    if (elem == 1)
+    const size_t rb = (size_t)W * elem;
+    const bool vec = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(dst) |
+                       ap | bp | dp | rb) & 15) == 0;
+    if (vec) {  // 16 bytes per thread; bytewise max >= min, so lane-wise 32-bit subtracts never borrow
+        const int vpr = (int)(rb / 16);
+        dim3 grid(cdiv(vpr, 64), cdiv(H, 4));
+        subtract16_kernel<<<grid, 256, 0, s>>>((const uint8_t*)a, ap, (const uint8_t*)b, bp, (uint8_t*)dst, dp, vpr, H);
+    } else if (elem == 1) {
+        dim3 grid(cdiv(W, 64), cdiv(H, 4));
         subtract_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)a, ap, (const uint8_t*)b, bp,
                                                        (uint8_t*)dst, dp, W, H);
-    else
+    } else {
+        dim3 grid(cdiv(W, 64), cdiv(H, 4));
         subtract_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)a, ap / 2, (const uint16_t*)b,
                                                         bp / 2, (uint16_t*)dst, dp / 2, W, H);
+    }
     count_launch();
     return cudaGetLastError();
 }
