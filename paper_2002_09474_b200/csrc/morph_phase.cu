@@ -110,13 +110,25 @@ bool choose(const MorphJob& j, Choice* c) {
     }
     c->pf = pf;
     c->smem = total;
-    // rows per item: ~4 items per resident CTA for balance, >= 4 warm-up lengths
-    const int occ = std::max(1, std::min(8, (228 * 1024) / (total + 1024)));
+    // rows per item: the persistent grid runs in waves of (SMs x resident CTAs) items; every item
+    // pays w1 warm-up rows plus a fixed switch cost. Pick the band count that minimises
+    // waves x (rows per item + w1 + 16): one full wave of long items beats many short ones
+    // (measured on 4096^2: 256-row items 15-30% faster than 64-row items).
+    const int occ = std::max(1, std::min(2, (228 * 1024) / (total + 1024)));
     const long strips = (long)((j.W + tw - 1) / tw) * j.batch;
-    const long target = 148L * occ * 4;
-    const long splits = std::max(1L, (target + strips - 1) / strips);
-    int rh = (int)((j.H + splits - 1) / splits);
-    rh = std::max(rh, std::min(j.H, std::max(64, 4 * w1)));
+    const long slots = 148L * occ;
+    long best_nb = 1;
+    double best_t = 1e30;
+    for (long nb = 1; nb <= std::max(1, j.H / 8); ++nb) {
+        const long rows = (j.H + nb - 1) / nb;
+        const long waves = (strips * nb + slots - 1) / slots;
+        const double t = (double)waves * (double)(rows + w1 + 16);
+        if (t < best_t - 1e-9) {
+            best_t = t;
+            best_nb = nb;
+        }
+    }
+    int rh = (int)((j.H + best_nb - 1) / best_nb);
     rh = (rh + 3) / 4 * 4;
     if (const char* e = getenv("RMGPU_STREAM_RH")) {
         const int v = atoi(e);
