@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "morph_col.cuh"
 
@@ -42,20 +43,10 @@ bool choose(const MorphJob& j, int* R) {
     const uintptr_t src0 = reinterpret_cast<uintptr_t>(j.src) - (uintptr_t)((size_t)j.above * j.sp);
     if ((src0 | j.sp | reinterpret_cast<uintptr_t>(j.dst) | j.dp) & 15) return false;
     if (j.batch > 1 && ((j.simg | j.dimg) & 15)) return false;
-    // rows per item: R + 2*gy a multiple of the block height (no half-used TMA boxes); about one
-    // item per resident warp (16 per SM) for small images, more for large ones
-    const long strips = (long)((j.W * j.elem + SB - 1) / SB) * j.batch;
-    const long warps = 148L * 16;
-    const long rows_per_warp = std::max(1L, ((long)j.H * strips + warps - 1) / warps);
-    int m = (int)std::max(2L, std::min(16L, (rows_per_warp + 2 * j.gy + BR - 1) / BR));
-    // small images: with two-block items fewer than half the resident warps would get work, so
-    // use single-block items (more warps in flight beats the extra halo rows)
-    if (m == 2 && BR - 2 * j.gy >= 4 && (long)((j.H + (2 * BR - 2 * j.gy) - 1) / (2 * BR - 2 * j.gy)) * strips < warps / 2)
-        m = 1;
-    if (const char* e = getenv("RMGPU_COL_BLOCKS")) m = std::max(1, atoi(e));
-    int r = m * BR - 2 * j.gy;
-    if (r < 1) r = BR;
-    *R = std::min(r, std::max(1, j.H));
+    // rows per item: chosen at launch from the kernel's occupancy (wave model, morph_col.cuh);
+    // RMGPU_COL_BLOCKS=m forces R = m * BR - 2 * gy (tuning)
+    *R = 0;
+    if (const char* e = getenv("RMGPU_COL_BLOCKS")) *R = std::max(1, atoi(e) * BR - 2 * j.gy);
     return true;
 }
 
@@ -81,7 +72,8 @@ const char* plan_name(const MorphJob& j) {
     k.simg = k.dimg = k.sp * j.H;
     int R = 0;
     if (!choose(k, &R)) return nullptr;
-    snprintf(buf, sizeof(buf), "col_%s_w%dx%d_R%d_smem%dK", j.elem == 1 ? "u8" : "u16", 2 * j.gx + 1, 2 * j.gy + 1, R,
+    snprintf(buf, sizeof(buf), "col_%s_w%dx%d_R%s_smem%dK", j.elem == 1 ? "u8" : "u16", 2 * j.gx + 1, 2 * j.gy + 1,
+             R > 0 ? std::to_string(R).c_str() : "auto",
              (j.gx == 0 ? ColGeo<0>::SMEM : ColGeo<1>::SMEM) / 1024);
     return buf;
 }

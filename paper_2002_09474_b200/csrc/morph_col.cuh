@@ -494,9 +494,7 @@ cudaError_t launch_col_variant(const MorphJob& j, int R) {
     p.simg = j.simg;
     p.dimg = j.dimg;
     p.batch = j.batch;
-    p.R = R;
     p.nstrips = cdiv(j.W * (int)sizeof(T), SB);
-    p.nbands = cdiv(j.H, R);
     CUtensorMap map;
     using CG = ColGeo<GX>;
     constexpr int SMEM = CG::SMEM;
@@ -509,6 +507,28 @@ cudaError_t launch_col_variant(const MorphJob& j, int R) {
     const int occ = kernel_occupancy((const void*)kern, WPB * 32, SMEM, &e);
     if (e != cudaSuccess) return e;
     const int sms = device_sm_count();
+    if (R <= 0) {
+        // rows per item (R + 2*GY a multiple of BR): the warps run in waves of (SMs x resident
+        // warps) items; minimise waves x (staged rows per item + a fixed switch cost)
+        const long slots = (long)sms * std::max(1, occ) * WPB;
+        const long strips = (long)p.nstrips * j.batch;
+        double best = 1e30;
+        for (int m = 1; m <= 64; ++m) {
+            const int r = m * BR - 2 * GY;
+            if (r < 1) continue;
+            const long items = strips * cdiv(j.H, r);
+            const long waves = (items + slots - 1) / slots;
+            const double t = (double)waves * (m * BR + 8);
+            if (t < best - 1e-9) {
+                best = t;
+                R = r;
+            }
+            if (r >= j.H) break;
+        }
+        R = std::min(R, std::max(1, j.H));
+    }
+    p.R = R;
+    p.nbands = cdiv(j.H, R);
     const long items = (long)p.nstrips * p.nbands * j.batch;
     const long ctas = std::max(1L, std::min((items + WPB - 1) / WPB, (long)sms * std::max(1, occ)));
     const long nwarps = ctas * WPB;
