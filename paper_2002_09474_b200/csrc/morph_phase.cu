@@ -65,7 +65,7 @@ bool choose(const MorphJob& j, Choice* c) {
             if (q > QMAX || !ok) continue;
             const int t = j.elem == 1 ? phase_smem<uint8_t>(hb0, B, q, 2) : phase_smem<uint16_t>(hb0, B, q, 2);
             if (t > 220 * 1024) continue;
-            const int occ = std::max(1, std::min(2, (228 * 1024) / (t + 1024)));
+            const int occ = std::max(1, std::min(phase_min_blocks(j.elem, B + 100 * r), (228 * 1024) / (t + 1024)));
             // vertical: min/max per output ~ 3 + (2r + q)/B (+ per-block overhead 6/B); horizontal:
             // one phase per chunk costs about the same wall time whether it has 5 or 8 row groups
             // (one warp each), so its per-row cost scales with 8 / (row groups per chunk)
@@ -114,7 +114,7 @@ bool choose(const MorphJob& j, Choice* c) {
     // pays w1 warm-up rows plus a fixed switch cost. Pick the band count that minimises
     // waves x (rows per item + w1 + 16): one full wave of long items beats many short ones
     // (measured on 4096^2: 256-row items 15-30% faster than 64-row items).
-    const int occ = std::max(1, std::min(2, (228 * 1024) / (total + 1024)));
+    const int occ = std::max(1, std::min(phase_min_blocks(j.elem, c->vb), (228 * 1024) / (total + 1024)));
     const long strips = (long)((j.W + tw - 1) / tw) * j.batch;
     const long slots = 148L * occ;
     long best_nb = 1;

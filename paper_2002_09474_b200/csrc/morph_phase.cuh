@@ -10,6 +10,9 @@ namespace phase {
 
 using namespace stream;
 
+// Register budget per variant: 3 resident CTAs per SM where the shared-memory footprint allows it
+// and the code fits 72 registers without spilling (u16, 8-row blocks); 2 (96 registers) otherwise.
+__host__ __device__ constexpr int phase_min_blocks(int elem, int vb) { return (elem == 2 || vb == 8) ? 3 : 2; }
 constexpr int PNT = 256;  // compute threads per CTA (every one runs both passes) + 1 producer warp
 constexpr int PNW = PNT / 32;
 
@@ -74,7 +77,7 @@ __device__ __forceinline__ int emitting_chunks(const Item& it, int KB) {
 }
 
 template <typename T, int MODE, int VB, int HB>
-__global__ void __launch_bounds__(PNT + 32, 2)
+__global__ void __launch_bounds__(PNT + 32, phase_min_blocks(sizeof(T), VB))
 morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tmap,
                    const __grid_constant__ CUtensorMap omap) {
     using G = SG<T>;
