@@ -301,6 +301,14 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
         for (int k = 0; k < QMAX; ++k) M[k] = IDV;
 
         for (int c0 = 0; c0 <= it.Lend; c0 += KB) {
+            // wx = 1: no horizontal pass -- the vertical results go straight into the output tile
+            // (row-major), so that tile must have been read out by its previous TMA store first
+            unsigned char* vout = nullptr;
+            if constexpr (HB == 1) {
+                const bool emitting = min(c0 + KB - 1, it.Lend) >= it.Lf;
+                vout = outbase + (size_t)(chunk & 1) * CH * OUTP;
+                if (emitting && chunk >= 2) mbar_wait(&oempty[chunk & 1], (uint32_t)((((chunk) >> 1) - 1) & 1));
+            }
             // ================= vertical phase: KB blocks of B rows into the transposed tile =========
             const int tci = chunk < 60 ? chunk : 59;
             if (warp == 0) RM_TRACE(tci * 8 + 0);
@@ -321,6 +329,19 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
                 const unsigned char* lead = sbase(sL);
                 uint32_t grp[GR];
                 auto flush = [&](int m0) {
+                    if constexpr (HB == 1) {
+                        // pixel pair (pos0, pos0+1) of GR rows -> output tile rows kb*B+m0+i
+                        const int pos0 = 2 * t - it.off;
+                        if (real && pos0 >= 0 && pos0 < TW) {
+#pragma unroll
+                            for (int i = 0; i < GR; ++i) {
+                                unsigned char* d = vout + (size_t)(kb * B + m0 + i) * OUTP + (size_t)pos0 * sz;
+                                if constexpr (sz == 1) *reinterpret_cast<uint16_t*>(d) = (uint16_t)prmt(grp[i], 0u, 0x0020);
+                                else *reinterpret_cast<uint32_t*>(d) = grp[i];
+                            }
+                        }
+                        return;
+                    }
                     unsigned char* rowg = vt + ((kb * B + m0) / GR) * VTG * ESZ;
                     if constexpr (sz == 1) {
                         *reinterpret_cast<uint2*>(rowg + voff0) =
@@ -386,14 +407,15 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
                 advance();
             }
             if (!emit_any) continue;  // warm-up chunk: nothing to hand over (uniform across the CTA)
+            const int oC = s + c0 * B - w1;  // output row of chunk row 0 (relative to the item)
+            const int ob = chunk & 1;
+            unsigned char* outt = outbase + (size_t)ob * CH * OUTP;
             if (warp == 0) RM_TRACE(tci * 8 + 3);
+            if constexpr (HB != 1) {
             bar_sync(BAR_C, PNT);  // transposed tile complete
             if (warp == 0) RM_TRACE(tci * 8 + 4);
 
             // ================= horizontal phase: one warp per row group ===============================
-            const int oC = s + c0 * B - w1;  // output row of chunk row 0 (relative to the item)
-            const int ob = chunk & 1;
-            unsigned char* outt = outbase + (size_t)ob * CH * OUTP;
             if (chunk >= 2) mbar_wait(&oempty[ob], (uint32_t)(((chunk >> 1) - 1) & 1));
             for (int g0 = warp * SUBG; g0 < NGC; g0 += PNW * SUBG) {
                 const int g = g0 + sub;
@@ -490,6 +512,7 @@ morph_phase_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tma
                     emit8(o);
                 }
             }
+            }  // HB != 1
             const int rlo = max(0, -oC), rhi = min(CH, it.rh - oC);
             const bool full_chunk = p.use_tma_out && rlo == 0 && rhi == CH && it.x0 + TW <= p.W;
             if (warp == 0) RM_TRACE(tci * 8 + 5);
