@@ -28,8 +28,7 @@ NVCC_FLAGS = ARCH + (["-DRMGPU_TRACE"] if os.environ.get("RMGPU_TRACE") else [])
                      "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
                      "-I", os.path.join(ROOT, "include")]
 CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_fast.cu", "morph_fast_u8_min.cu", "morph_fast_u8_max.cu",
-              "morph_fast_u16_min.cu", "morph_fast_u16_max.cu", "morph_stream.cu", "morph_stream_u8_min.cu",
-              "morph_stream_u8_max.cu", "morph_stream_u16_min.cu", "morph_stream_u16_max.cu", "morph_phase.cu",
+              "morph_fast_u16_min.cu", "morph_fast_u16_max.cu", "morph_stream.cu", "morph_phase.cu",
               "morph_phase_u8_min.cu", "morph_phase_u8_max.cu", "morph_phase_u16_min.cu", "morph_phase_u16_max.cu",
               "morph_col.cu", "morph_col_u8_min.cu", "morph_col_u8_max.cu", "morph_col_u16_min.cu",
               "morph_col_u16_max.cu", "morph_col_u8_grad.cu", "morph_col_u16_grad.cu", "transpose.cu",

@@ -90,16 +90,11 @@ namespace {
 
 thread_local std::string t_last_error;
 // Test / tuning hooks: RMGPU_DISABLE_STREAM=1 routes around the TMA kernels (exercises the
-// fallbacks); RMGPU_KERNEL=stream prefers the warp-specialised kernel over the phase kernel.
+// fallback kernels).
 const bool g_disable_stream = [] {
     const char* v = getenv("RMGPU_DISABLE_STREAM");
     return v && v[0] == '1';
 }();
-const bool g_prefer_stream = [] {
-    const char* v = getenv("RMGPU_KERNEL");
-    return v && v[0] == 's';
-}();
-
 int fail(int status, const std::string& msg) {
     t_last_error = msg;
     return status;
@@ -213,15 +208,15 @@ int run_single(MorphJob j) {
         return RMGPU_OK;
     }
     cudaError_t e = cudaSuccess;
-    if (!g_disable_stream && !g_prefer_stream && rmgpu::col::launch(j, &e)) {
+    if (!g_disable_stream && rmgpu::col::launch(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "register-streaming morph kernel");
         return RMGPU_OK;
     }
-    if (!g_disable_stream && !g_prefer_stream && rmgpu::phase::launch(j, &e)) {
+    if (!g_disable_stream && rmgpu::phase::launch(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "phase morph kernel");
         return RMGPU_OK;
     }
-    if (j.mode == rmgpu::MODE_GRAD && !g_disable_stream && !g_prefer_stream) {
+    if (j.mode == rmgpu::MODE_GRAD && !g_disable_stream) {
         // large-window gradient: dilation into scratch and erosion into dst with the phase kernel,
         // then dst = dilation - erosion (dispatch.cpp:58-71; never negative, no wrap)
         const size_t rb = (size_t)j.W * j.elem, tp = (rb + 255) & ~size_t(255), timg = tp * (size_t)j.H;
@@ -248,10 +243,6 @@ int run_single(MorphJob j) {
             return rc;
         }
         cudaFreeAsync(hi, j.stream);
-    }
-    if (!g_disable_stream && rmgpu::stream::launch(j, &e)) {
-        if (e != cudaSuccess) return cuda_fail(e, "stream morph kernel");
-        return RMGPU_OK;
     }
     if (rmgpu::launch_fast(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "fast morph kernel");
@@ -472,11 +463,11 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
     j.mode = op == RMGPU_ERODE ? rmgpu::MODE_MIN : op == RMGPU_DILATE ? rmgpu::MODE_MAX : rmgpu::MODE_GRAD;
     if (op == RMGPU_OPEN || op == RMGPU_CLOSE) j.mode = rmgpu::MODE_MIN;
     if (j.gx == 0 && j.gy == 0) return "copy";
-    if (!g_disable_stream && !g_prefer_stream)
+    if (!g_disable_stream)
         if (const char* n = rmgpu::col::plan_name(j)) return n;
-    if (!g_disable_stream && !g_prefer_stream)
+    if (!g_disable_stream)
         if (const char* n = rmgpu::phase::plan_name(j)) return n;
-    if (j.mode == rmgpu::MODE_GRAD && !g_disable_stream && !g_prefer_stream) {
+    if (j.mode == rmgpu::MODE_GRAD && !g_disable_stream) {
         MorphJob m = j;
         m.mode = rmgpu::MODE_MAX;
         if (const char* n = rmgpu::phase::plan_name(m)) {
@@ -485,8 +476,6 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
             return g.c_str();
         }
     }
-    if (!g_disable_stream)
-        if (const char* n = rmgpu::stream::plan_name(j)) return n;
     if (const char* n = rmgpu::fast_plan_name(j)) return n;
     if (rmgpu::generic_tile_fits(j)) return "generic_tile";
     return "two_pass_global";

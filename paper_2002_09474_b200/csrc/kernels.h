@@ -47,11 +47,9 @@ cudaError_t launch_subtract(const void* a, size_t ap, const void* b, size_t bp, 
 bool launch_fast(const MorphJob& j, cudaError_t* err);
 const char* fast_plan_name(const MorphJob& j);
 
-// ---- strip-streaming fused path (morph_stream.cu), preferred over launch_fast ------------------
+// ---- shared TMA infrastructure (morph_stream.cu) -----------------------------------------------
 namespace stream {
-bool launch(const MorphJob& j, cudaError_t* err);
-const char* plan_name(const MorphJob& j);
-void set_trace(long long* device_buf, int cta);  // debug timeline (tools/trace_stream.py)
+void set_trace(long long* device_buf, int cta);  // debug timeline of the phase kernel (tools/trace_phase.py)
 }  // namespace stream
 
 // ---- persistent phase-based fused path (morph_phase.cu), preferred over the streaming one -----
