@@ -228,6 +228,56 @@ def test_row_bands_with_halo(gpu, restatement, op):
                 assert np.array_equal(out, want), (op, dtype, border, nb)
 
 
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_aligned_batches_and_bands_fuzz(gpu, restatement, dtype):
+    # 16-byte aligned pitches and image strides, so batches and row bands (explicit halo rows)
+    # go through the TMA kernels (K1 for w <= 7, K2 otherwise): every op, both borders
+    import torch
+    rng = np.random.default_rng(99 + np.dtype(dtype).itemsize)
+    mx = int(np.iinfo(dtype).max)
+    es = np.dtype(dtype).itemsize
+    kinds = set()
+    for c in range(120):
+        w = int(rng.integers(1, 700))
+        h = int(rng.integers(1, 300))
+        small = c % 2 == 0
+        wx = int(2 * rng.integers(0, 4 if small else 40) + 1)
+        wy = int(2 * rng.integers(0, 4 if small else 40) + 1)
+        op = int(rng.integers(0, 5))
+        border = int(rng.integers(0, 2))
+        bval = int(rng.integers(0, mx + 1))
+        pad = (-w) % (16 // es)
+        if c % 4 < 2:  # batch of independent images
+            nb = int(rng.integers(2, 5))
+            imgs = np.stack([restatement.generate(w, h, 500 + 10 * c + b, stream=b, dtype=dtype) for b in range(nb)])
+            src = to_device(imgs, pad)
+            dst = empty_device(imgs.shape, dtype, pad)
+            gpu.morph_batched_device(src, dst, wx, wy, op, border, bval)
+            torch.cuda.synchronize()
+            got = to_host(dst)
+            for b in range(nb):
+                want = restatement.morph(imgs[b], wx, wy, op, border, bval)
+                assert np.array_equal(got[b], want), ("batch", c, b, w, h, wx, wy, op, border)
+        else:  # row bands with real halo rows, as the multi-GPU split uses them
+            img = restatement.generate(w, h, 900 + c, dtype=dtype)
+            want = restatement.morph(img, wx, wy, op, border, bval)
+            halo = (wy // 2) * (2 if op in (OPEN, CLOSE) else 1)
+            nbands = int(rng.integers(1, 5))
+            out = np.zeros_like(img)
+            for k in range(nbands):
+                r0, r1 = h * k // nbands, h * (k + 1) // nbands
+                if r1 == r0:
+                    continue
+                a, z = max(0, r0 - halo), min(h, r1 + halo)
+                src = to_device(img[a:z], pad)
+                dst = empty_device((r1 - r0, w), dtype, pad)
+                gpu.morph_band_device(src, r0 - a, z - r1, dst, wx, wy, op, border, bval)
+                out[r0:r1] = to_host(dst)
+            assert np.array_equal(out, want), ("bands", c, w, h, wx, wy, op, border, nbands)
+        kinds.add(gpu.plan_name(es, w, h, wx, wy, op).split("_")[0])
+    assert {"col", "phase"} <= kinds, kinds
+
+
 def test_transpose_images(gpu, restatement):
     import torch
     for dtype in (np.uint8, np.uint16):
