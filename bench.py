@@ -581,9 +581,16 @@ def main(argv=None):
                     for sd in side:
                         sd.wait_event(fork)
                     lanes = [cap] + side
-                    for k, (_, spec, _, _) in enumerate(wl.ops):
-                        with torch.cuda.stream(lanes[k % len(lanes)]):
-                            wl.launch(spec)
+                    nl = len(lanes)
+                    # lane i takes ops i, i+nl, ...; odd lanes walk their share in reverse so that
+                    # concurrently running kernels differ (small-window K1 beside large-window K2)
+                    for i, lane_s in enumerate(lanes):
+                        share = list(range(i, len(wl.ops), nl))
+                        if i % 2:
+                            share.reverse()
+                        with torch.cuda.stream(lane_s):
+                            for k in share:
+                                wl.launch(wl.ops[k][1])
                     for sd in side:
                         ev = torch.cuda.Event()
                         ev.record(sd)
