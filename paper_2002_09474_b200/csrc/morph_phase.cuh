@@ -576,8 +576,6 @@ cudaError_t launch_phase_variant(const MorphJob& j, int rh, int B, int q, int pf
     p.batch = j.batch;
     p.trace = g_trace;
     p.trace_cta = g_trace_cta;
-    static const int sleep_ns = getenv("RMGPU_PHASE_SLEEP") ? atoi(getenv("RMGPU_PHASE_SLEEP")) : 100;
-    p.sleep_ns = sleep_ns;
     CUtensorMap map, omap;
     p.use_tma = encode_input_map(j, HG<T, HB>::RP / 4, B, &map) ? 1 : 0;
     p.use_tma_out = encode_output_map(j, G::TW * (int)sizeof(T), chunk_rows(B), &omap) ? 1 : 0;

@@ -145,7 +145,6 @@ struct StreamParams {
     int use_tma;          // interior blocks through one 2-D tensor copy (map rows start at row_lo)
     int use_tma_out;      // full output chunks through one TMA tensor store
     int batch;            // images
-    int sleep_ns;         // phase kernel: producer back-off when it has nothing to issue
 };
 
 #ifdef RMGPU_TRACE
