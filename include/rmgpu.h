@@ -175,6 +175,9 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
 /* Debug: clock64 timeline of one CTA of the streaming kernel into a device buffer of >= 1024
  * int64 (NULL disables). Not part of the reference API. */
 void rmgpu_debug_trace(void* device_buf, int cta);
+/* Debug / tuning: override a planner knob (e.g. "sep_rb", "sep_pf", "sep_parts", "sep_notma",
+ * "sep"; value < 0 removes the override). Knobs never change results. Not part of the reference API. */
+void rmgpu_debug_set(const char* knob, int value);
 
 #ifdef __cplusplus
 }

@@ -46,6 +46,7 @@ SIGNATURES = {
     "rmgpu_launch_count": [],
     "rmgpu_plan_name": [_I, _I, _I, _I, _I, _I],
     "rmgpu_debug_trace": [_P, _I],
+    "rmgpu_debug_set": [C.c_char_p, _I],
 }
 _RESTYPES = {
     "rmgpu_last_error": C.c_char_p,
@@ -53,6 +54,7 @@ _RESTYPES = {
     "rmgpu_launch_count": C.c_ulonglong,
     "rmgpu_plan_name": C.c_char_p,
     "rmgpu_debug_trace": None,
+    "rmgpu_debug_set": None,
 }
 
 _lock = threading.Lock()

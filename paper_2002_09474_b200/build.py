@@ -31,7 +31,9 @@ CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_fast.cu", "morph_fast_u8_min
               "morph_fast_u16_min.cu", "morph_fast_u16_max.cu", "morph_stream.cu", "morph_phase.cu",
               "morph_phase_u8_min.cu", "morph_phase_u8_max.cu", "morph_phase_u16_min.cu", "morph_phase_u16_max.cu",
               "morph_col.cu", "morph_col_u8_min.cu", "morph_col_u8_max.cu", "morph_col_u16_min.cu",
-              "morph_col_u16_max.cu", "morph_col_u8_grad.cu", "morph_col_u16_grad.cu", "transpose.cu",
+              "morph_col_u16_max.cu", "morph_col_u8_grad.cu", "morph_col_u16_grad.cu", "morph_sep.cu",
+              "morph_sep_h_u8_min.cu", "morph_sep_h_u8_max.cu", "morph_sep_h_u16_min.cu", "morph_sep_h_u16_max.cu",
+              "transpose.cu",
               "generate.cu"]
 HOST_SOURCES = [os.path.join("host", "rectmorph_b200.cpp")]
 
@@ -47,6 +49,27 @@ def _headers() -> list[str]:
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     hs.append(os.path.join(ROOT, "include", "rmgpu.h"))
     return hs
+
+
+def _deps(path: str, seen: set | None = None) -> set:
+    """Local headers a source includes, transitively (#include "..." resolved in csrc/ or include/)."""
+    seen = set() if seen is None else seen
+    try:
+        lines = open(path).read().splitlines()
+    except OSError:
+        return seen
+    for ln in lines:
+        ln = ln.strip()
+        if ln.startswith("#include") and '"' in ln:
+            name = ln.split('"')[1]
+            for d in (os.path.dirname(path), CSRC, os.path.join(ROOT, "include")):
+                h = os.path.normpath(os.path.join(d, name))
+                if os.path.exists(h):
+                    if h not in seen:
+                        seen.add(h)
+                        _deps(h, seen)
+                    break
+    return seen
 
 
 def _run(cmd: list[str]) -> None:
@@ -68,7 +91,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src.replace(".cu", ".o"))
         objs.append(o)
-        if force or _newer(o, [s] + headers):
+        if force or _newer(o, [s] + sorted(_deps(s))):
             jobs.append([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o])
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(_run, jobs))

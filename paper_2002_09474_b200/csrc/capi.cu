@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -43,6 +44,23 @@ std::unordered_map<OccKey, int, OccHash> g_occ;
 std::unordered_map<OccKey, int, OccHash> g_smem_set;  // (kern, dev) -> dynamic smem limit set so far
 int g_sms[64];
 }  // namespace
+
+namespace {
+std::mutex g_tune_mu;
+std::map<std::string, int> g_tune;
+}  // namespace
+
+int tune(const char* name, int dflt) {
+    {
+        std::lock_guard<std::mutex> g(g_tune_mu);
+        auto it = g_tune.find(name);
+        if (it != g_tune.end()) return it->second;
+    }
+    std::string env = "RMGPU_";
+    for (const char* c = name; *c; ++c) env += (char)toupper((unsigned char)*c);
+    const char* v = getenv(env.c_str());
+    return v ? atoi(v) : dflt;
+}
 
 int kernel_occupancy(const void* kern, int threads, int smem, cudaError_t* err) {
     int dev = 0;
@@ -210,6 +228,16 @@ int run_single(MorphJob j) {
     cudaError_t e = cudaSuccess;
     if (!g_disable_stream && rmgpu::col::launch(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "register-streaming morph kernel");
+        return RMGPU_OK;
+    }
+    if (!g_disable_stream && rmgpu::sep::applicable(j)) {
+        const size_t tb = rmgpu::sep::scratch_bytes(j);
+        void* tmp = nullptr;
+        if (tb) RM_CUDA(scratch_alloc(&tmp, tb, j.stream));
+        e = rmgpu::sep::run(j, tmp);
+        cudaError_t fe = tb ? cudaFreeAsync(tmp, j.stream) : cudaSuccess;
+        if (e != cudaSuccess) return cuda_fail(e, "separable streaming passes");
+        if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
         return RMGPU_OK;
     }
     if (!g_disable_stream && rmgpu::phase::launch(j, &e)) {
@@ -449,6 +477,13 @@ unsigned long long rmgpu_launch_count(void) { return rmgpu::g_launch_count.load(
 // >= 1024 int64 (nullptr disables). Not part of the reference API.
 void rmgpu_debug_trace(void* device_buf, int cta) { rmgpu::stream::set_trace((long long*)device_buf, cta); }
 
+void rmgpu_debug_set(const char* knob, int value) {
+    if (!knob) return;
+    std::lock_guard<std::mutex> g(rmgpu::g_tune_mu);
+    if (value < 0) rmgpu::g_tune.erase(knob);
+    else rmgpu::g_tune[knob] = value;
+}
+
 int rmgpu_resolve(int algo, int window, int axis, int threshold_h, int threshold_v) {
     if (algo != RMGPU_ALGO_AUTO) return algo;  // dispatch.cpp:14-20
     const int t = axis == RMGPU_AXIS_HORIZONTAL ? threshold_h : threshold_v;
@@ -465,6 +500,8 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
     if (j.gx == 0 && j.gy == 0) return "copy";
     if (!g_disable_stream)
         if (const char* n = rmgpu::col::plan_name(j)) return n;
+    if (!g_disable_stream)
+        if (const char* n = rmgpu::sep::plan_name(j)) return n;
     if (!g_disable_stream)
         if (const char* n = rmgpu::phase::plan_name(j)) return n;
     if (j.mode == rmgpu::MODE_GRAD && !g_disable_stream) {

@@ -31,6 +31,9 @@ struct MorphJob {
 // per SM (0 and an error on failure).
 int kernel_occupancy(const void* kern, int threads, int smem, cudaError_t* err);
 int device_sm_count();
+// Planner knob: the rmgpu_debug_set override if any, else the environment variable RMGPU_<NAME>
+// (upper-cased), else dflt.
+int tune(const char* name, int dflt);
 
 // ---- generic paths (morph_generic.cu): any window, any pitch --------------------------------
 bool generic_tile_fits(const MorphJob& j);
@@ -63,6 +66,14 @@ namespace col {
 bool launch(const MorphJob& j, cudaError_t* err);
 const char* plan_name(const MorphJob& j);
 }  // namespace col
+
+// ---- K3: vertical and horizontal streaming passes handing over through L2 (morph_sep.cu) ------
+namespace sep {
+bool applicable(const MorphJob& j);
+size_t scratch_bytes(const MorphJob& j);  // 0: no intermediate (one axis has window 1)
+cudaError_t run(const MorphJob& j, void* tmp);
+const char* plan_name(const MorphJob& j);
+}  // namespace sep
 
 // ---- transposes (transpose.cu) ---------------------------------------------------------------
 cudaError_t launch_transpose(const void* src, size_t sp, void* dst, size_t dp, int W, int H,

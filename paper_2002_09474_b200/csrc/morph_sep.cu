@@ -1,0 +1,256 @@
+// morph_sep.cu -- planner and launchers of K3 (morph_sep.cuh): vertical pass V and horizontal pass H
+// as two streaming kernels with the intermediate handed over through L2 (row bands sized so that
+// one band of the intermediate stays resident). Reference semantics: separable.cpp:130-157 (V then
+// H, window 1 = identity), image.cpp:58-66 (replicate / constant borders per axis).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "morph_sep.cuh"
+
+namespace rmgpu {
+namespace sep {
+
+cudaError_t launch_h_u8_min(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
+cudaError_t launch_h_u8_max(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
+cudaError_t launch_h_u16_min(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
+cudaError_t launch_h_u16_max(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
+
+namespace {
+
+constexpr int QM = 8;
+constexpr int kBlocks[] = {8, 10, 12, 14, 16, 18, 20, 22, 24};
+
+int env_int(const char* name, int dflt) { return tune(name, dflt); }
+
+// V block size B: the tail r = 2g mod B must be <= VRMAX (folded from re-read rows), q-1 <= QM
+// block minima in registers; per output row the pass folds (q-1 + r)/B extra values and larger B
+// costs registers (u16 keeps B <= 16).
+bool choose_b(int elem, int g, int* B_out) {
+    const int w1 = 2 * g;
+    double best = 1e30;
+    int bb = 0;
+    for (int B : kBlocks) {
+        if (B > w1 || (elem == 2 && B > 16)) continue;
+        const int q = w1 / B, r = w1 % B;
+        if (r > VRMAX || q - 1 > QM) continue;
+        const double cost = (0.5 * (q - 1) + r) / B + 0.01 * B;
+        if (cost < best) {
+            best = cost;
+            bb = B;
+        }
+    }
+    *B_out = bb;
+    return bb != 0;
+}
+
+// H chunk width for a wing g: C = 16 for u8 wings >= 8, 8 otherwise (>= 4); at most 8 halo lanes.
+bool choose_c(int elem, int g, int* C_out) {
+    int C;
+    if (elem == 1) C = g >= 8 ? 16 : 8;
+    else C = 8;
+    if (g < C / 2) return false;
+    const int A = g / C + (g % C ? 1 : 0);
+    if (A > 8) return false;
+    *C_out = C;
+    return true;
+}
+
+// TMA-fed variant when the maps encode (16-byte pitches); the plain LDG kernel otherwise.
+template <typename T, int MODE, int B>
+cudaError_t launch_v_t(const SepParams& p0, dim3 grid, cudaStream_t s, const MorphJob& j) {
+    constexpr int sz = sizeof(T), SB = 128 * sz;
+    SepParams p = p0;
+    CUtensorMap lmap, tmap, omap;
+    // the TMA pipeline pays off on large images (16384^2 u8 1x63: 77% vs 65% of HBM); on small ones
+    // the plain-load kernel ramps faster (4096^2: 13.0 vs 15.4 us)
+    const long long px = (long long)j.W * j.H * j.batch;
+    const int no_tma = env_int("sep_notma", px >= (1LL << 26) ? 0 : 1);
+    bool tma = !no_tma && stream::encode_input_map(j, SB / 4, B, &lmap) &&
+               stream::encode_input_map(j, SB / 4, B + VRMAX, &tmap) && stream::encode_output_map(j, SB, B, &omap);
+    if (tma) {
+        const int pf = std::max(1, env_int("sep_pf", 1));
+        p.nsl = p.nst = pf + 1;
+        p.wsmem = ((p.nsl * B + p.nst * (B + VRMAX) + 2 * B) * SB + 8 * (p.nsl + p.nst) + 127) / 128 * 128;
+        p.nstrips = (p.nwords + 31) / 32;
+        p.nbands = (int)grid.y;
+        const long long warps = (long long)p.nstrips * p.nbands * p.batch;
+        auto kern = vtma_kernel<T, MODE, B, QM>;
+        cudaError_t e = cudaSuccess;
+        const int smem = VTW * p.wsmem;
+        kernel_occupancy((const void*)kern, VT, smem, &e);
+        if (e != cudaSuccess) return e;
+        kern<<<dim3((unsigned)((warps + VTW - 1) / VTW)), VT, smem, s>>>(p, lmap, tmap, omap);
+    } else {
+        vpass_kernel<T, MODE, B, QM><<<grid, VT, 0, s>>>(p);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename T, int MODE>
+cudaError_t launch_v_b(const SepParams& p, int B, dim3 grid, cudaStream_t s, const MorphJob& j) {
+    switch (B) {
+#define RM_V(BB) \
+    case BB: return launch_v_t<T, MODE, BB>(p, grid, s, j);
+        RM_V(8) RM_V(10) RM_V(12) RM_V(14) RM_V(16) RM_V(18) RM_V(20) RM_V(22) RM_V(24)
+#undef RM_V
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_v(const SepParams& p, int elem, int mode, int B, dim3 grid, cudaStream_t s, const MorphJob& j) {
+    if (elem == 1) return mode == MODE_MIN ? launch_v_b<uint8_t, MODE_MIN>(p, B, grid, s, j) : launch_v_b<uint8_t, MODE_MAX>(p, B, grid, s, j);
+    return mode == MODE_MIN ? launch_v_b<uint16_t, MODE_MIN>(p, B, grid, s, j) : launch_v_b<uint16_t, MODE_MAX>(p, B, grid, s, j);
+}
+
+cudaError_t launch_h(const SepParams& p, int elem, int mode, int C, dim3 grid, cudaStream_t s) {
+    const int bx = p.g % C;
+    if (elem == 1) return mode == MODE_MIN ? launch_h_u8_min(p, C, bx, grid, s) : launch_h_u8_max(p, C, bx, grid, s);
+    return mode == MODE_MIN ? launch_h_u16_min(p, C, bx, grid, s) : launch_h_u16_max(p, C, bx, grid, s);
+}
+
+SepParams base_params(const MorphJob& j) {
+    SepParams p{};
+    p.W = j.W;
+    p.H = j.H;
+    p.cmode = j.cmode;
+    p.bval = j.bval;
+    p.batch = j.batch;
+    return p;
+}
+
+// One vertical pass over the job's rows: src (rows [-above, H + below) valid) -> out.
+cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg) {
+    int B = 0;
+    if (!choose_b(j.elem, j.gy, &B)) return cudaErrorInvalidValue;
+    SepParams p = base_params(j);
+    p.src = static_cast<const uint8_t*>(j.src);
+    p.sp = j.sp;
+    p.simg = j.simg;
+    p.dst = static_cast<uint8_t*>(out);
+    p.dp = op;
+    p.dimg = oimg;
+    p.row_lo = -j.above;
+    p.row_hi = j.H + j.below;
+    p.g = j.gy;
+    p.q = 2 * j.gy / B;
+    p.r = 2 * j.gy % B;
+    p.nwords = (j.W + 3) / 4;
+    // bands: ~24 resident warps per SM; the warm-up (q-1 blocks per band) stays < ~50% of a band
+    const long long cols = (long long)p.nwords * j.batch;
+    const int sms = device_sm_count();
+    int bands = (int)std::max(1LL, ((long long)sms * 24 * 32 + cols - 1) / cols);
+    int rb = (j.H + bands - 1) / bands;
+    rb = std::max(rb, 2 * (p.q - 1) * B);
+    if ((long long)j.W * j.H * j.batch >= (1LL << 26)) rb = std::max(rb, 320);  // TMA path: long bands
+    rb = env_int("sep_rb", rb);
+    rb = std::max(B, (rb + B - 1) / B * B);
+    p.rb = rb;
+    const dim3 grid((unsigned)((p.nwords + VT - 1) / VT), (unsigned)((j.H + rb - 1) / rb), (unsigned)j.batch);
+    MorphJob jo = j;  // the output side of the tensor maps
+    jo.dst = out;
+    jo.dp = op;
+    jo.dimg = oimg;
+    return launch_v(p, j.elem, j.mode, B, grid, j.stream, jo);
+}
+
+// One horizontal pass over H rows: in -> job dst.
+cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int discard) {
+    int C = 0;
+    if (!choose_c(j.elem, j.gx, &C)) return cudaErrorInvalidValue;
+    SepParams p = base_params(j);
+    p.src = static_cast<const uint8_t*>(in);
+    p.sp = ip;
+    p.simg = iimg;
+    p.dst = static_cast<uint8_t*>(j.dst);
+    p.dp = j.dp;
+    p.dimg = j.dimg;
+    p.g = j.gx;
+    p.groups = (j.H + 3) / 4;
+    p.discard = discard;
+    // parts: ~24 resident warps per SM, each part a whole number of segments
+    const int A = j.gx / C + (j.gx % C ? 1 : 0);
+    const int OS = (32 - 2 * A) * C;
+    const int nseg = (j.W + OS - 1) / OS;
+    const long long rowsw = (long long)p.groups * j.batch;
+    // each warp keeps one segment in flight: parts of <= 8 segments (measured: 4096^2 u8 63x1 best
+    // at 2 parts, 16384^2 at 4-5)
+    int parts = (nseg + 7) / 8;
+    parts = std::min(std::max(1, env_int("sep_parts", parts)), nseg);
+    const int segs_per = (nseg + parts - 1) / parts;
+    p.pw = segs_per * OS;
+    p.parts = (nseg + segs_per - 1) / segs_per;
+    const long long warps = rowsw * p.parts;
+    const dim3 grid((unsigned)((warps + HT / 32 - 1) / (HT / 32)));
+    return launch_h(p, j.elem, j.mode, C, grid, j.stream);
+}
+
+}  // namespace
+
+bool applicable(const MorphJob& j) {
+    const int enabled = env_int("sep", 1);
+    if (!enabled) return false;
+    if (j.mode != MODE_MIN && j.mode != MODE_MAX) return false;
+    if (j.elem != 1 && j.elem != 2) return false;
+    if (j.W < 1 || j.H < 1) return false;
+    if ((reinterpret_cast<uintptr_t>(j.src) | reinterpret_cast<uintptr_t>(j.dst) | j.sp | j.dp |
+         (j.batch > 1 ? (j.simg | j.dimg) : 0)) & 15)
+        return false;
+    if (j.gx == 0 && j.gy == 0) return false;
+    int t;
+    if (j.gy != 0 && !choose_b(j.elem, j.gy, &t)) return false;
+    if (j.gx != 0 && !choose_c(j.elem, j.gx, &t)) return false;
+    return true;
+}
+
+size_t scratch_pitch(const MorphJob& j) { return ((size_t)j.W * j.elem + 255) & ~size_t(255); }
+
+// Rows per L2 band of the intermediate (the whole image when it fits).
+int band_rows(const MorphJob& j) {
+    const size_t budget = (size_t)env_int("sep_l2mb", 40) << 20;
+    const size_t per_row = scratch_pitch(j) * (size_t)j.batch;
+    const long long rows = std::max<long long>(64, (long long)(budget / std::max<size_t>(per_row, 1)));
+    return (int)std::min<long long>(rows, j.H);
+}
+
+cudaError_t run(const MorphJob& j, void* tmp) {
+    if (j.gy == 0) return run_h(j, j.src, j.sp, j.simg, 0);
+    if (j.gx == 0) return run_v(j, j.dst, j.dp, j.dimg);
+    const size_t tp = scratch_pitch(j);
+    const int R = band_rows(j);
+    const size_t timg = tp * (size_t)R;
+    for (int y0 = 0; y0 < j.H; y0 += R) {
+        MorphJob b = j;
+        const int rows = std::min(R, j.H - y0);
+        b.src = static_cast<const uint8_t*>(j.src) + (size_t)y0 * j.sp;
+        b.dst = static_cast<uint8_t*>(j.dst) + (size_t)y0 * j.dp;
+        b.H = rows;
+        b.above = j.above + y0;
+        b.below = j.below + (j.H - y0 - rows);
+        cudaError_t e = run_v(b, tmp, tp, timg);
+        if (e != cudaSuccess) return e;
+        e = run_h(b, tmp, tp, timg, 1);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+size_t scratch_bytes(const MorphJob& j) {
+    if (j.gx == 0 || j.gy == 0) return 0;
+    return scratch_pitch(j) * (size_t)band_rows(j) * (size_t)j.batch;
+}
+
+const char* plan_name(const MorphJob& j) {
+    static thread_local char buf[96];
+    if (!applicable(j)) return nullptr;
+    int B = 0, C = 0;
+    if (j.gy) choose_b(j.elem, j.gy, &B);
+    if (j.gx) choose_c(j.elem, j.gx, &C);
+    snprintf(buf, sizeof buf, "sep_%s_vB%d_hC%d_band%d", j.elem == 1 ? "u8" : "u16", B, C,
+             (j.gx && j.gy) ? band_rows(j) : 0);
+    return buf;
+}
+
+}  // namespace sep
+}  // namespace rmgpu

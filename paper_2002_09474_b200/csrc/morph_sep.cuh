@@ -1,0 +1,651 @@
+// morph_sep.cuh -- K3: the separable rectangle as two streaming passes that hand over through L2.
+//
+// The reference computes a w_x x w_y erosion/dilation as a vertical pass into a full intermediate
+// image followed by a horizontal pass (separable.cpp:130-157; van Herk / Gil-Werman for long
+// windows, sliding_extrema.cpp:58-132). On B200 the intermediate of a 4096^2 u8 image (16 MB) fits
+// the 126 MB L2 many times over, so K3 keeps the reference's two-pass structure and makes each pass
+// a barrier-free, shared-memory-free streaming kernel:
+//
+//  * V (vertical pass): one thread per 4-pixel column word streams down a band of rows with
+//    plain coalesced loads. Block van Herk with blocks of B rows: out = min3(T[m], G, P[m]) where
+//    P is the running prefix of the leading block, T the suffix of the trailing rows (re-read: they
+//    were loaded w_y rows earlier and are still in L2) and G the minimum of the q-1 whole blocks in
+//    between (block minima kept in registers). Nothing is staged in shared memory.
+//  * H (horizontal pass): one warp per group of 4 rows sweeps the row in segments of 32 lane
+//    chunks of C columns. Each lane transposes its 4 x C pixels in registers (PRMT) so that the two
+//    16-bit lanes of a word hold different ROWS of one column, scans prefix and suffix along its C
+//    columns, and fetches the far suffix / prefix / chunk minima from the lanes a = g / C away with
+//    SHFL (g mod C is a template parameter, so every register index is compile-time).
+//  * Pixels use 16-bit SIMD lanes (VIMNMX(3).U16x2). u8 words keep their raw bytes: the 16-bit
+//    min/max of raw words is exact in the high byte of each lane, so a word A = raw carries pixels
+//    1 and 3 and A << 8 carries pixels 0 and 2 (no unpacking; one PRMT repacks).
+//
+// The intermediate is a private scratch buffer: the H pass discards every line it has finished
+// with (discard.global.L2), so it is never written back to HBM. HBM traffic = 1 read of the input
+// + 1 write of the output, the algorithmic minimum.
+#pragma once
+
+#include "morph_stream.cuh"  // TMA / mbarrier helpers, tensor-map encoders
+
+namespace rmgpu {
+namespace sep {
+
+struct SepParams {
+    const uint8_t* src;
+    size_t sp;
+    uint8_t* dst;
+    size_t dp;
+    int W, H;            // output extent of one image
+    int row_lo, row_hi;  // V: valid input rows relative to output row 0 ([-above, H + below))
+    int g;               // wing along the pass axis
+    int q, r;            // V: 2g = q*B + r
+    int rb;              // V: output rows per band (multiple of B)
+    int cmode;
+    uint32_t bval;
+    size_t simg, dimg;
+    int nwords;          // V: 4-pixel column words per row
+    int groups;          // H: 4-row groups per image
+    int parts, pw;       // H: column parts per row group (one warp each), output columns per part
+    int batch;
+    int discard;         // H: discard the source lines after use (source = private scratch)
+    int nstrips, nbands; // V (TMA): 128-pixel strips per row, bands per image
+    int nsl, nst;        // V (TMA): leading / trailing ring slots per warp
+    int wsmem;           // V (TMA): shared-memory bytes per warp
+};
+
+// 4 pixels of one row (V) in two 16-bit-lane words.
+template <typename T>
+struct W4;
+template <>
+struct W4<uint8_t> {
+    static __device__ __forceinline__ uint2 load(const uint8_t* p) {
+        const uint32_t raw = __ldg(reinterpret_cast<const unsigned int*>(p));
+        return make_uint2(raw, raw << 8);
+    }
+    static __device__ __forceinline__ void store(uint8_t* p, uint2 v) {
+        *reinterpret_cast<uint32_t*>(p) = prmt(v.x, v.y, 0x3715);
+    }
+    static __device__ __forceinline__ uint2 splat(uint32_t b) {
+        const uint32_t w = b * 0x01010101u;
+        return make_uint2(w, w);
+    }
+    static __device__ __forceinline__ uint32_t pixel(uint2 v, int k) {  // pixel k of a word pair
+        return k & 1 ? (v.x >> (8 * k)) & 0xFF : (v.y >> (8 * k + 8)) & 0xFF;
+    }
+};
+template <>
+struct W4<uint16_t> {
+    static __device__ __forceinline__ uint2 load(const uint8_t* p) {
+        return __ldg(reinterpret_cast<const uint2*>(p));
+    }
+    static __device__ __forceinline__ void store(uint8_t* p, uint2 v) { *reinterpret_cast<uint2*>(p) = v; }
+    static __device__ __forceinline__ uint2 splat(uint32_t b) {
+        const uint32_t w = b * 0x00010001u;
+        return make_uint2(w, w);
+    }
+    static __device__ __forceinline__ uint32_t pixel(uint2 v, int k) {
+        const uint32_t w = k < 2 ? v.x : v.y;
+        return (w >> (16 * (k & 1))) & 0xFFFF;
+    }
+};
+
+template <int MODE>
+__device__ __forceinline__ uint2 op2(uint2 a, uint2 b) {
+    return make_uint2(red2_u16x2<MODE>(a.x, b.x), red2_u16x2<MODE>(a.y, b.y));
+}
+template <int MODE>
+__device__ __forceinline__ uint2 op3(uint2 a, uint2 b, uint2 c) {
+    return make_uint2(red3_u16x2<MODE>(a.x, b.x, c.x), red3_u16x2<MODE>(a.y, b.y, c.y));
+}
+template <int MODE>
+__device__ __forceinline__ uint2 ident2() {
+    const uint32_t v = MODE == MODE_MIN ? 0xFFFFFFFFu : 0u;
+    return make_uint2(v, v);
+}
+
+constexpr int VT = 128;  // threads per V block
+constexpr int HT = 128;  // threads per H block (4 warps, one 4-row group each)
+
+// ================================ V: vertical pass ==============================================
+// Raw row words: u8 = one 32-bit word (4 pixels), u16 = two (4 pixels).
+template <typename T>
+struct VW;
+template <>
+struct VW<uint8_t> {
+    using Raw = uint32_t;
+    static __device__ __forceinline__ Raw load(const uint8_t* p) { return __ldg(reinterpret_cast<const unsigned int*>(p)); }
+    static __device__ __forceinline__ uint2 unpack(Raw r) { return make_uint2(r, r << 8); }
+    static __device__ __forceinline__ Raw splat(uint32_t b) { return b * 0x01010101u; }
+    static __device__ __forceinline__ Raw sel(bool c, Raw a, Raw b) { return c ? a : b; }
+};
+template <>
+struct VW<uint16_t> {
+    using Raw = uint2;
+    static __device__ __forceinline__ Raw load(const uint8_t* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+    static __device__ __forceinline__ uint2 unpack(Raw r) { return r; }
+    static __device__ __forceinline__ Raw splat(uint32_t b) { return make_uint2(b * 0x00010001u, b * 0x00010001u); }
+    static __device__ __forceinline__ Raw sel(bool c, Raw a, Raw b) { return make_uint2(c ? a.x : b.x, c ? a.y : b.y); }
+};
+
+// Ragged last column word (W % 4 != 0): the pixels past W are computed from in-pitch garbage and
+// dropped here, one pixel store each.
+template <typename T>
+__device__ __forceinline__ void store_partial(uint8_t* p, uint2 v, int n) {
+    for (int k = 0; k < n; ++k) reinterpret_cast<T*>(p)[k] = (T)W4<T>::pixel(v, k);
+}
+
+constexpr int VRMAX = 4;  // tail rows r = 2g mod B folded from re-read rows (planner keeps r <= 4)
+
+// One block of B output rows. Window of output m (leading input row base+m):
+//   rows [base+m-2g, base+m] = T[m] u G u P[m] with
+//   T[m] = suffix of the trailing batch [base-2g, base-2g+B) from m,
+//   G    = the r rows [base-2g+B, base-(q-1)B) u whole blocks L-q+1 .. L-1 (minima M[0..q-2]),
+//   P[m] = prefix of the leading block [base, base+m].
+// All 2B (+r) loads are issued before the first reduction (no branches between them).
+template <typename T, int MODE, int B, int QM, bool EDGE, bool FULL>
+__device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uint8_t* drow, int base, int nst,
+                                       int nvalid, uint2 (&M)[QM]) {
+    using V = VW<T>;
+    using Raw = typename V::Raw;
+    const int w1 = 2 * p.g, q = p.q, r = p.r;
+    const uint2 ID = ident2<MODE>();
+    const Raw CW = V::splat(p.bval);
+    const ptrdiff_t sp = (ptrdiff_t)p.sp;
+    auto ldE = [&](int i) -> Raw {  // border-aware (edge bands): clamp, then substitute the constant
+        const int ic = min(max(i, p.row_lo), p.row_hi - 1);
+        const Raw v = V::load(s + (ptrdiff_t)ic * sp);
+        return V::sel(p.cmode && ic != i, CW, v);
+    };
+    Raw xt[B], xl[B], xr[VRMAX];
+    const int tb = base - w1;                    // first trailing row
+    const int rb0 = base - (q - 1) * B - r;      // first of the r tail rows
+    if constexpr (EDGE) {
+#pragma unroll
+        for (int m = 0; m < B; ++m) xt[m] = ldE(tb + m);
+#pragma unroll
+        for (int t = 0; t < VRMAX; ++t)
+            if (t < r) xr[t] = ldE(rb0 + t);
+#pragma unroll
+        for (int m = 0; m < B; ++m) xl[m] = ldE(base + m);
+    } else {
+        const uint8_t* pt = s + (ptrdiff_t)tb * sp;
+#pragma unroll
+        for (int m = 0; m < B; ++m) xt[m] = V::load(pt + m * sp);
+        const uint8_t* pr = s + (ptrdiff_t)rb0 * sp;
+#pragma unroll
+        for (int t = 0; t < VRMAX; ++t)
+            if (t < r) xr[t] = V::load(pr + t * sp);
+        const uint8_t* pl = s + (ptrdiff_t)base * sp;
+#pragma unroll
+        for (int m = 0; m < B; ++m) xl[m] = V::load(pl + m * sp);
+    }
+    uint2 Tm[B];
+    uint2 acc = V::unpack(xt[B - 1]);
+    Tm[B - 1] = acc;
+#pragma unroll
+    for (int m = B - 2; m >= 0; --m) {
+        acc = op2<MODE>(acc, V::unpack(xt[m]));
+        Tm[m] = acc;
+    }
+    uint2 G = ID;
+#pragma unroll
+    for (int t = 0; t < VRMAX; ++t) G = op2<MODE>(G, t < r ? V::unpack(xr[t]) : ID);
+#pragma unroll
+    for (int k = 0; k + 1 < QM; k += 2) G = op3<MODE>(G, k < q - 1 ? M[k] : ID, k + 1 < q - 1 ? M[k + 1] : ID);
+    uint2 P = ID;
+#pragma unroll
+    for (int m = 0; m < B; ++m) {
+        P = op2<MODE>(P, V::unpack(xl[m]));
+        const uint2 o = op3<MODE>(Tm[m], G, P);
+        uint8_t* d = drow + (ptrdiff_t)m * (ptrdiff_t)p.dp;
+        if constexpr (FULL) {
+            W4<T>::store(d, o);
+        } else if (m < nst) {
+            if (nvalid == 4) W4<T>::store(d, o);
+            else store_partial<T>(d, o, nvalid);
+        }
+    }
+#pragma unroll
+    for (int k = QM - 1; k > 0; --k) M[k] = M[k - 1];
+    M[0] = P;
+}
+
+template <typename T, int MODE, int B, int QM, bool EDGE>
+__device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s, uint8_t* d, int y0, int y1,
+                                           int nvalid) {
+    using V = VW<T>;
+    const int i0 = y0 + p.g;  // leading input row of output row y0
+    const uint2 ID = ident2<MODE>();
+    uint2 M[QM];
+#pragma unroll
+    for (int k = 0; k < QM; ++k) M[k] = ID;
+    // warm-up: minima of the q-1 whole blocks before block 0
+    for (int L = -(p.q - 1); L < 0; ++L) {
+        const int base = i0 + L * B;
+        typename V::Raw x[B];
+#pragma unroll
+        for (int m = 0; m < B; ++m) {
+            int i = base + m;
+            if constexpr (EDGE) {
+                const int ic = min(max(i, p.row_lo), p.row_hi - 1);
+                x[m] = V::sel(p.cmode && ic != i, V::splat(p.bval), V::load(s + (ptrdiff_t)ic * (ptrdiff_t)p.sp));
+            } else {
+                x[m] = V::load(s + (ptrdiff_t)i * (ptrdiff_t)p.sp);
+            }
+        }
+        uint2 P = V::unpack(x[0]);
+#pragma unroll
+        for (int m = 1; m < B; ++m) P = op2<MODE>(P, V::unpack(x[m]));
+#pragma unroll
+        for (int k = QM - 1; k > 0; --k) M[k] = M[k - 1];
+        M[0] = P;
+    }
+    for (int yb = y0; yb < y1; yb += B) {
+        const int base = i0 + (yb - y0);
+        uint8_t* drow = d + (ptrdiff_t)yb * (ptrdiff_t)p.dp;
+        const int nst = y1 - yb;
+        if (nst >= B && nvalid == 4) vblock<T, MODE, B, QM, EDGE, true>(p, s, drow, base, nst, nvalid, M);
+        else vblock<T, MODE, B, QM, EDGE, false>(p, s, drow, base, nst, nvalid, M);
+    }
+}
+
+template <typename T, int MODE, int B, int QM>
+__global__ void __launch_bounds__(VT) vpass_kernel(const SepParams p) {
+    const int c = blockIdx.x * VT + threadIdx.x;
+    if (c >= p.nwords) return;
+    const int y0 = blockIdx.y * p.rb;
+    const int y1 = min(y0 + p.rb, p.H);
+    const int nblk = (y1 - y0 + B - 1) / B;
+    constexpr int sz = sizeof(T);
+    const uint8_t* s = p.src + (size_t)blockIdx.z * p.simg + (size_t)c * 4 * sz;
+    uint8_t* d = p.dst + (size_t)blockIdx.z * p.dimg + (size_t)c * 4 * sz;
+    // rows touched: [y0 - g, y0 + nblk*B - 1 + g]
+    const bool edge = (y0 - p.g < p.row_lo) || (y0 + nblk * B + p.g > p.row_hi);
+    const int nvalid = min(4, p.W - 4 * c);
+    if (edge) vpass_body<T, MODE, B, QM, true>(p, s, d, y0, y1, nvalid);
+    else vpass_body<T, MODE, B, QM, false>(p, s, d, y0, y1, nvalid);
+}
+
+// ---------------- V fed by TMA: one warp = one strip of 128 pixels x one band ------------------
+// Every warp is an independent pipeline (no CTA barriers): lane 0 streams the leading blocks (B
+// rows) and the trailing batches (B + VRMAX rows, L2 hits) into two private shared-memory rings with
+// 2-D TMA boxes, PF blocks ahead; all lanes read rows with one LDS each (compile-time offsets, no
+// address arithmetic) and write results into a double-buffered output tile that leaves through
+// one TMA tensor store per block. Bands touching the image border take the LDG path above.
+constexpr int VTW = VT / 32;  // warps per CTA
+
+template <typename T, int MODE, int B, int QM>
+__global__ void __launch_bounds__(VT) vtma_kernel(const SepParams p, const __grid_constant__ CUtensorMap lmap,
+                                                  const __grid_constant__ CUtensorMap tmap,
+                                                  const __grid_constant__ CUtensorMap omap) {
+    using V = VW<T>;
+    using Raw = typename V::Raw;
+    using namespace stream;
+    constexpr int sz = sizeof(T);
+    constexpr int SB = 128 * sz;  // bytes per strip row
+    constexpr int TB = B + VRMAX;  // rows per trailing box
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * VTW + warp;
+    const int per_img = p.nstrips * p.nbands;
+    const int img = wid / per_img;
+    if (img >= p.batch) return;
+    const int rem = wid - img * per_img;
+    const int band = rem / p.nstrips;
+    const int strip = rem - band * p.nstrips;
+    const int y0 = band * p.rb;
+    const int y1 = min(y0 + p.rb, p.H);
+    const int nblk = (y1 - y0 + B - 1) / B;
+    const int g = p.g, w1 = 2 * g, q = p.q, r = p.r;
+    // bands whose rows reach past the valid input rows fill the rings themselves (clamped rows /
+    // the constant), synchronously; everything downstream is shared with the TMA path
+    const bool edge = (y0 - g < p.row_lo) || (y0 + nblk * B + g > p.row_hi);
+    const uint8_t* ecol = p.src + (size_t)img * p.simg + (size_t)min(strip * 32 + lane, p.nwords - 1) * 4 * sz;
+    auto fill = [&](unsigned char* slot, int row0, int nrows) {
+        const Raw CW = V::splat(p.bval);
+        for (int m = 0; m < nrows; ++m) {
+            const int i = row0 + m;
+            const int ic = min(max(i, p.row_lo), p.row_hi - 1);
+            const Raw v = V::load(ecol + (ptrdiff_t)ic * (ptrdiff_t)p.sp);
+            *reinterpret_cast<Raw*>(slot + m * SB + lane * 4 * sz) = V::sel(p.cmode && ic != i, CW, v);
+        }
+        __syncwarp();
+    };
+    const int NSL = p.nsl, NST = p.nst;
+    unsigned char* wbase = smem + (size_t)warp * p.wsmem;
+    unsigned char* lring = wbase;
+    unsigned char* tring = lring + (size_t)NSL * B * SB;
+    unsigned char* outb = tring + (size_t)NST * TB * SB;
+    uint64_t* fl = reinterpret_cast<uint64_t*>(outb + 2 * B * SB);
+    uint64_t* ft = fl + NSL;
+    if (lane == 0) {
+        for (int k = 0; k < NSL; ++k) mbar_init(&fl[k], 1);
+        for (int k = 0; k < NST; ++k) mbar_init(&ft[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    const int i0 = y0 + g;  // leading input row of output row y0
+    const int nL = q - 1 + nblk;
+    const int xw = strip * (SB / 4);  // map x coordinate (32-bit words)
+    auto issue_lead = [&](int jl, int slot) {
+        mbar_arrive_tx(&fl[slot], (uint32_t)(B * SB));
+        tma_box(lring + (size_t)slot * B * SB, &lmap, xw, i0 + (jl - (q - 1)) * B - p.row_lo, img, &fl[slot]);
+    };
+    auto issue_trail = [&](int L, int slot) {
+        mbar_arrive_tx(&ft[slot], (uint32_t)(TB * SB));
+        tma_box(tring + (size_t)slot * TB * SB, &tmap, xw, i0 + L * B - w1 - p.row_lo, img, &ft[slot]);
+    };
+    if (lane == 0 && !edge) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&lmap) : "memory");
+        for (int k = 0; k < NSL && k < nL; ++k) issue_lead(k, k);
+        for (int k = 0; k < NST && k < nblk; ++k) issue_trail(k, k);
+    }
+    const uint2 ID = ident2<MODE>();
+    uint2 M[QM];
+#pragma unroll
+    for (int k = 0; k < QM; ++k) M[k] = ID;
+    const int lo = lane * 4 * sz;
+    int lslot = 0, lpar = 0, tslot = 0, tpar = 0;  // ring positions of block jl / L
+    for (int jl = 0; jl < nL; ++jl) {
+        const int L = jl - (q - 1);
+        unsigned char* lsb = lring + (size_t)lslot * B * SB;
+        const unsigned char* ls = lsb + lo;
+        if (edge) fill(lsb, i0 + L * B, B);
+        else mbar_wait(&fl[lslot], (uint32_t)lpar);
+        if (L < 0) {  // warm-up block: its minimum only
+            uint2 P = V::unpack(*reinterpret_cast<const Raw*>(ls));
+#pragma unroll
+            for (int m = 1; m < B; ++m) P = op2<MODE>(P, V::unpack(*reinterpret_cast<const Raw*>(ls + m * SB)));
+#pragma unroll
+            for (int k = QM - 1; k > 0; --k) M[k] = M[k - 1];
+            M[0] = P;
+            __syncwarp();
+            if (lane == 0 && !edge && jl + NSL < nL) issue_lead(jl + NSL, lslot);
+            if (++lslot == NSL) { lslot = 0; lpar ^= 1; }
+            continue;
+        }
+        unsigned char* tsb = tring + (size_t)tslot * TB * SB;
+        const unsigned char* ts = tsb + lo;
+        if (edge) fill(tsb, i0 + L * B - w1, TB);
+        else mbar_wait(&ft[tslot], (uint32_t)tpar);
+        uint2 Tm[B];
+        uint2 acc = V::unpack(*reinterpret_cast<const Raw*>(ts + (B - 1) * SB));
+        Tm[B - 1] = acc;
+#pragma unroll
+        for (int m = B - 2; m >= 0; --m) {
+            acc = op2<MODE>(acc, V::unpack(*reinterpret_cast<const Raw*>(ts + m * SB)));
+            Tm[m] = acc;
+        }
+        uint2 G = ID;
+#pragma unroll
+        for (int t = 0; t < VRMAX; ++t)
+            G = op2<MODE>(G, t < r ? V::unpack(*reinterpret_cast<const Raw*>(ts + (B + t) * SB)) : ID);
+#pragma unroll
+        for (int k = 0; k + 1 < QM; k += 2) G = op3<MODE>(G, k < q - 1 ? M[k] : ID, k + 1 < q - 1 ? M[k + 1] : ID);
+        // output tile L & 1: its previous TMA store (block L-2) must have finished reading it
+        unsigned char* obb = outb + (size_t)(L & 1) * B * SB;
+        unsigned char* ob = obb + lo;
+        if (L >= 2) {
+            if (lane == 0) bulk_wait_read1();
+            __syncwarp();
+        }
+        uint2 P = ID;
+#pragma unroll
+        for (int m = 0; m < B; ++m) {
+            P = op2<MODE>(P, V::unpack(*reinterpret_cast<const Raw*>(ls + m * SB)));
+            W4<T>::store(ob + m * SB, op3<MODE>(Tm[m], G, P));
+        }
+#pragma unroll
+        for (int k = QM - 1; k > 0; --k) M[k] = M[k - 1];
+        M[0] = P;
+        fence_async_smem();  // the tile's generic writes before the async-proxy store reads it
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_box(&omap, strip * SB, y0 + L * B, img, obb);
+            bulk_commit();
+            if (!edge && jl + NSL < nL) issue_lead(jl + NSL, lslot);
+            if (!edge && L + NST < nblk) issue_trail(L + NST, tslot);
+        }
+        if (++lslot == NSL) { lslot = 0; lpar ^= 1; }
+        if (++tslot == NST) { tslot = 0; tpar ^= 1; }
+    }
+    if (lane == 0) bulk_wait_all();
+}
+
+// ================================ H: horizontal pass ============================================
+// Lane chunk geometry: C columns x 4 rows per lane. u8: C = 16 (16-byte row loads) or 8; u16: 8.
+template <typename T, int C>
+struct HChunk {
+    static constexpr int sz = sizeof(T);
+    static constexpr int RB = C * sz;        // bytes per row per lane
+    static constexpr int NW = RB / 4;        // 32-bit words per row per lane
+};
+
+template <typename T, int C>
+__device__ __forceinline__ void h_load_row(const uint8_t* p, uint32_t (&w)[HChunk<T, C>::NW]) {
+    constexpr int NW = HChunk<T, C>::NW;
+    if constexpr (NW == 4) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    } else {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+        w[0] = v.x; w[1] = v.y;
+    }
+}
+template <typename T, int C>
+__device__ __forceinline__ void h_store_row(uint8_t* p, const uint32_t (&w)[HChunk<T, C>::NW]) {
+    constexpr int NW = HChunk<T, C>::NW;
+    if constexpr (NW == 4) *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    else *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+}
+
+// Border-aware load of one lane chunk row (chunks that reach past column 0 or W-1). Chunks start
+// at multiples of C, so a chunk is either wholly left of the image, wholly right of it, or holds
+// the last n < C real pixels followed by border pixels.
+template <typename T, int C>
+__device__ __forceinline__ void h_load_row_edge(const uint8_t* row, int cx, int W, int cmode, uint32_t bval,
+                                                uint32_t (&w)[HChunk<T, C>::NW]) {
+    constexpr int sz = sizeof(T);
+    constexpr int NW = HChunk<T, C>::NW;
+    const T* rp = reinterpret_cast<const T*>(row);
+    const uint32_t splat = sz == 1 ? 0x01010101u : 0x00010001u;
+    if (cx + C <= 0 || cx >= W) {
+        const uint32_t v = cmode ? bval : (uint32_t)rp[cx < 0 ? 0 : W - 1];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) w[k] = v * splat;
+        return;
+    }
+    h_load_row<T, C>(row + (ptrdiff_t)cx * sz, w);
+    const uint32_t rep = (cmode ? bval : (uint32_t)rp[W - 1]) * splat;
+    const int nb = (W - cx) * sz;  // real bytes in the chunk (< C * sz)
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+        const int kb = nb - 4 * k;
+        const uint32_t keep = kb >= 4 ? 0xFFFFFFFFu : (kb <= 0 ? 0u : (1u << (8 * kb)) - 1u);
+        w[k] = (w[k] & keep) | (rep & ~keep);
+    }
+}
+
+// rows r0..r3 (NW words each) -> per column c: {A, B} 16-bit-lane words holding 4 rows
+template <typename T, int C>
+__device__ __forceinline__ void h_transpose_in(const uint32_t (&r0)[HChunk<T, C>::NW],
+                                               const uint32_t (&r1)[HChunk<T, C>::NW],
+                                               const uint32_t (&r2)[HChunk<T, C>::NW],
+                                               const uint32_t (&r3)[HChunk<T, C>::NW], uint2 (&x)[C]) {
+    if constexpr (sizeof(T) == 1) {
+        // A = {row1 -> byte1, row3 -> byte3}, B = {row0 -> byte1, row2 -> byte3}
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int k = c >> 2, e = c & 3;
+            const uint32_t sel = (uint32_t)(e << 4) | (uint32_t)((4 + e) << 12);
+            x[c].x = prmt(r1[k], r3[k], sel);
+            x[c].y = prmt(r0[k], r2[k], sel);
+        }
+    } else {
+        // A = {row0, row1}, B = {row2, row3}
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int k = c >> 1;
+            const uint32_t sel = (c & 1) ? 0x7632u : 0x5410u;
+            x[c].x = prmt(r0[k], r1[k], sel);
+            x[c].y = prmt(r2[k], r3[k], sel);
+        }
+    }
+}
+
+template <typename T, int C>
+__device__ __forceinline__ void h_transpose_out(const uint2 (&o)[C], uint32_t (&r0)[HChunk<T, C>::NW],
+                                                uint32_t (&r1)[HChunk<T, C>::NW], uint32_t (&r2)[HChunk<T, C>::NW],
+                                                uint32_t (&r3)[HChunk<T, C>::NW]) {
+    if constexpr (sizeof(T) == 1) {
+#pragma unroll
+        for (int k = 0; k < C / 4; ++k) {
+            const uint2 a = o[4 * k], b = o[4 * k + 1], c = o[4 * k + 2], e = o[4 * k + 3];
+            // B words: byte1 = row0, byte3 = row2; A words: byte1 = row1, byte3 = row3
+            const uint32_t b01 = prmt(a.y, b.y, 0x7351), b23 = prmt(c.y, e.y, 0x7351);
+            const uint32_t a01 = prmt(a.x, b.x, 0x7351), a23 = prmt(c.x, e.x, 0x7351);
+            r0[k] = prmt(b01, b23, 0x5410);
+            r2[k] = prmt(b01, b23, 0x7632);
+            r1[k] = prmt(a01, a23, 0x5410);
+            r3[k] = prmt(a01, a23, 0x7632);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < C / 2; ++k) {
+            const uint2 a = o[2 * k], b = o[2 * k + 1];
+            r0[k] = prmt(a.x, b.x, 0x5410);
+            r1[k] = prmt(a.x, b.x, 0x7632);
+            r2[k] = prmt(a.y, b.y, 0x5410);
+            r3[k] = prmt(a.y, b.y, 0x7632);
+        }
+    }
+}
+
+__device__ __forceinline__ uint2 shup(uint2 v, int d) {
+    return make_uint2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+__device__ __forceinline__ uint2 shdn(uint2 v, int d) {
+    return make_uint2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
+}
+
+// One warp = one group of 4 rows; segments of 32 lane chunks; BX = g mod C (compile-time).
+// The next segment's rows are loaded before the current one is reduced (one segment in flight).
+template <typename T, int MODE, int C, int BX>
+__global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
+    using HC = HChunk<T, C>;
+    constexpr int NW = HC::NW, sz = sizeof(T);
+    const int lane = threadIdx.x & 31;
+    const int widx = blockIdx.x * (HT / 32) + (threadIdx.x >> 5);
+    const int gidx = widx / p.parts;
+    const int part = widx - gidx * p.parts;
+    const int img = gidx / p.groups;
+    const int grp = gidx - img * p.groups;
+    if (img >= p.batch) return;  // whole warp: no shuffle partner is left behind
+    const int a = p.g / C;                   // whole chunks in the wing
+    const int A = a + (BX > 0 ? 1 : 0);      // halo lanes on each side
+    const int OS = (32 - 2 * A) * C;         // output columns per segment
+    const int W = p.W;
+    const int y = grp * 4;
+    const int nrows = min(4, p.H - y);
+    const uint8_t* sb = p.src + (size_t)img * p.simg;
+    uint8_t* db = p.dst + (size_t)img * p.dimg;
+    const uint8_t* srow0 = sb + (size_t)y * p.sp;
+    // rows past H (last group) re-read row H-1; their results are never stored
+    const size_t rs1 = nrows > 1 ? p.sp : 0, rs2 = nrows > 2 ? 2 * p.sp : rs1, rs3 = nrows > 3 ? 3 * p.sp : rs2;
+    const uint2 ID = ident2<MODE>();
+
+    uint32_t r0[NW], r1[NW], r2[NW], r3[NW];
+    auto load_seg = [&](int X) {
+        const int cx = X + (lane - A) * C;
+        if (cx >= 0 && cx + C <= W) {
+            const uint8_t* b = srow0 + (ptrdiff_t)cx * sz;
+            h_load_row<T, C>(b, r0);
+            h_load_row<T, C>(b + rs1, r1);
+            h_load_row<T, C>(b + rs2, r2);
+            h_load_row<T, C>(b + rs3, r3);
+        } else {
+            h_load_row_edge<T, C>(srow0, cx, W, p.cmode, p.bval, r0);
+            h_load_row_edge<T, C>(srow0 + rs1, cx, W, p.cmode, p.bval, r1);
+            h_load_row_edge<T, C>(srow0 + rs2, cx, W, p.cmode, p.bval, r2);
+            h_load_row_edge<T, C>(srow0 + rs3, cx, W, p.cmode, p.bval, r3);
+        }
+    };
+    const int xlo = part * p.pw, xhi = min(W, xlo + p.pw);
+    load_seg(xlo);
+    for (int X = xlo; X < xhi; X += OS) {
+        const int cx = X + (lane - A) * C;  // first column of this lane's chunk
+        uint2 x[C];
+        h_transpose_in<T, C>(r0, r1, r2, r3, x);
+        if (X + OS < xhi) load_seg(X + OS);
+        uint2 P[C], S[C];
+        P[0] = x[0];
+#pragma unroll
+        for (int c = 1; c < C; ++c) P[c] = op2<MODE>(P[c - 1], x[c]);
+        S[C - 1] = x[C - 1];
+#pragma unroll
+        for (int c = C - 2; c >= 0; --c) S[c] = op2<MODE>(S[c + 1], x[c]);
+        const uint2 cm = P[C - 1];
+        // chunk minima strictly inside the window: lanes L-a+1 .. L+a-1, plus lane L-a when the
+        // left end lies one chunk further out (dl) and lane L+a when the right end does (dr)
+        uint2 base = a > 0 ? cm : ID;
+        for (int dd = 1; dd < a; ++dd) base = op3<MODE>(base, shup(cm, dd), shdn(cm, dd));
+        const uint2 ml = shup(cm, a), mr = shdn(cm, a);
+        uint2 m00 = base, m10, m01, m11;
+        if (a > 0) {
+            m10 = op2<MODE>(base, ml);
+            m01 = op2<MODE>(base, mr);
+            m11 = op3<MODE>(base, ml, mr);
+        } else {  // a = 0: only both ends one chunk out leave a whole chunk (this lane's) inside
+            m10 = ID;
+            m01 = ID;
+            m11 = cm;
+        }
+        uint2 o[C];
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            const bool dl = j < BX;       // left end in chunk L-a-1
+            const bool dr = j + BX >= C;  // right end in chunk L+a+1
+            const uint2 sl = shup(S[(j - BX + C) % C], a + (dl ? 1 : 0));
+            const uint2 pr = shdn(P[(j + BX) % C], a + (dr ? 1 : 0));
+            const uint2 mid = dl ? (dr ? m11 : m10) : (dr ? m01 : m00);
+            o[j] = op3<MODE>(sl, mid, pr);
+        }
+        uint32_t o0[NW], o1[NW], o2[NW], o3[NW];
+        h_transpose_out<T, C>(o, o0, o1, o2, o3);
+        if (lane >= A && lane < 32 - A && cx < W) {
+            uint8_t* drow = db + (size_t)y * p.dp + (ptrdiff_t)cx * sz;
+            if (cx + C <= W) {
+                h_store_row<T, C>(drow, o0);
+                if (nrows > 1) h_store_row<T, C>(drow + p.dp, o1);
+                if (nrows > 2) h_store_row<T, C>(drow + 2 * p.dp, o2);
+                if (nrows > 3) h_store_row<T, C>(drow + 3 * p.dp, o3);
+            } else {
+                const int n = W - cx;
+                auto part = [&](int k, const uint32_t (&rw)[NW]) {
+                    if (k < nrows)
+                        for (int e = 0; e < n; ++e)
+                            reinterpret_cast<T*>(drow + (size_t)k * p.dp)[e] = (T)(rw[(e * sz) / 4] >> ((e * sz * 8) & 31));
+                };
+                part(0, o0);
+                part(1, o1);
+                part(2, o2);
+                part(3, o3);
+            }
+        }
+    }
+    if (p.discard) {
+        // drop the source lines only this warp reads (its part minus the halos the neighbouring
+        // parts read) from L2 unwritten: the source is a private scratch band
+        __syncwarp();
+        const int elo = part == 0 ? 0 : xlo + A * C;
+        const int ehi = part == p.parts - 1 ? W : xhi - A * C;
+        const int l0 = part == 0 ? 0 : (elo * sz + 127) / 128;
+        const int l1 = part == p.parts - 1 ? (W * sz + 127) / 128 : (ehi * sz) / 128;
+        for (int k = 0; k < nrows; ++k)
+            for (int l = l0 + lane; l < l1; l += 32)
+                asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(srow0 + (size_t)k * p.sp + (size_t)l * 128) : "memory");
+    }
+}
+
+}  // namespace sep
+}  // namespace rmgpu
