@@ -368,5 +368,11 @@ def launch_count() -> int:
     return int(lib().rmgpu_launch_count())
 
 
+def debug_set(knob: str, value: int) -> None:
+    """Override a planner tuning knob (rmgpu_debug_set); value < 0 removes the override. Knobs
+    choose kernel variants / launch geometry only, never results."""
+    lib().rmgpu_debug_set(knob.encode(), int(value))
+
+
 def plan_name(elem_bytes: int, w: int, h: int, wx: int, wy: int, op: int = ERODE) -> str:
     return lib().rmgpu_plan_name(elem_bytes, w, h, wx, wy, op).decode()

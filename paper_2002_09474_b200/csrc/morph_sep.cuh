@@ -251,6 +251,7 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
 
 template <typename T, int MODE, int B, int QM>
 __global__ void __launch_bounds__(VT) vpass_kernel(const SepParams p) {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // H may start scheduling
     const int c = blockIdx.x * VT + threadIdx.x;
     if (c >= p.nwords) return;
     const int y0 = blockIdx.y * p.rb;
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(VT) vtma_kernel(const SepParams p, const __gri
     constexpr int SB = 128 * sz;  // bytes per strip row
     constexpr int TB = B + VRMAX;  // rows per trailing box
     extern __shared__ __align__(128) unsigned char smem[];
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // H may start scheduling
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wid = blockIdx.x * VTW + warp;
     const int per_img = p.nstrips * p.nbands;
@@ -540,6 +542,7 @@ __global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
     const int part = widx - gidx * p.parts;
     const int img = gidx / p.groups;
     const int grp = gidx - img * p.groups;
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // no-op unless launched as a PDL dependent
     if (img >= p.batch) return;  // whole warp: no shuffle partner is left behind
     const int a = p.g / C;                   // whole chunks in the wing
     const int A = a + (BX > 0 ? 1 : 0);      // halo lanes on each side
@@ -645,6 +648,25 @@ __global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
             for (int l = l0 + lane; l < l1; l += 32)
                 asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(srow0 + (size_t)k * p.sp + (size_t)l * 128) : "memory");
     }
+}
+
+// H launch: after a V pass into the scratch band (p.discard) H is a programmatic dependent launch
+// -- its CTAs are scheduled while V's last wave drains and wait (griddepcontrol.wait) for V's
+// results before reading them.
+inline cudaError_t launch_hk(void (*kern)(SepParams), const SepParams& p, dim3 grid, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(HT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = p.discard && tune("sep_pdl", 1) ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace sep

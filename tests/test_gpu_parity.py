@@ -275,7 +275,76 @@ def test_aligned_batches_and_bands_fuzz(gpu, restatement, dtype):
                 out[r0:r1] = to_host(dst)
             assert np.array_equal(out, want), ("bands", c, w, h, wx, wy, op, border, nbands)
         kinds.add(gpu.plan_name(es, w, h, wx, wy, op).split("_")[0])
-    assert {"col", "phase"} <= kinds, kinds
+    assert {"col", "sep"} <= kinds, kinds
+
+
+SEP_KNOBS = [
+    {},                                   # planner defaults
+    {"sep_notma": 0, "sep_pf": 1},        # TMA-fed vertical pass on small images (one slot ahead)
+    {"sep_notma": 0, "sep_pf": 3, "sep_rb": 24},  # deeper TMA prefetch, short bands (more edge bands)
+    {"sep_notma": 1, "sep_rb": 8},        # plain-load vertical pass, one block per band
+    {"sep_l2mb": 0, "sep_parts": 3},      # intermediate in 64-row L2 bands, 3 warps per row group
+    {"sep_parts": 1, "sep_pdl": 0},       # one warp per row group, no programmatic dependent launch
+]
+
+
+@pytest.mark.parametrize("knobs", range(len(SEP_KNOBS)))
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_sep_passes_fuzz(gpu, restatement, dtype, knobs):
+    # K3 (separable streaming passes through L2) under every planner knob that changes its launch
+    # geometry: every chunk class g mod C, block size / tail r, edge bands, ragged words, batches
+    # and row bands, both borders
+    import torch
+    rng = np.random.default_rng(1234 + 7 * knobs + np.dtype(dtype).itemsize)
+    mx = int(np.iinfo(dtype).max)
+    es = np.dtype(dtype).itemsize
+    for k, v in SEP_KNOBS[knobs].items():
+        gpu.debug_set(k, v)
+    try:
+        seen = set()
+        for c in range(48):
+            w = int(rng.integers(1, 900))
+            h = int(rng.integers(1, 400))
+            g = [0, int(rng.integers(4, 70)), int(rng.integers(4, 20))]
+            wx = 2 * g[int(rng.integers(0, 3))] + 1 if c % 6 else 2 * int(rng.integers(4, 16)) + 1
+            wy = 2 * g[int(rng.integers(0, 3))] + 1 if c % 5 else 1
+            if wx == 1 and wy == 1:
+                wx = 2 * int(rng.integers(4, 40)) + 1
+            op = int(rng.integers(0, 2))
+            border = int(rng.integers(0, 2))
+            bval = int(rng.integers(0, mx + 1))
+            pad = (-w) % (16 // es) + 16 // es * int(rng.integers(0, 3))
+            if c % 3 == 0:
+                nb = int(rng.integers(2, 4))
+                imgs = np.stack([restatement.generate(w, h, 70 + 10 * c + b, stream=b, dtype=dtype) for b in range(nb)])
+                src = to_device(imgs, pad)
+                dst = empty_device(imgs.shape, dtype, pad)
+                gpu.morph_batched_device(src, dst, wx, wy, op, border, bval)
+                torch.cuda.synchronize()
+                got = to_host(dst)
+                for b in range(nb):
+                    want = restatement.morph(imgs[b], wx, wy, op, border, bval)
+                    assert np.array_equal(got[b], want), ("batch", knobs, c, b, w, h, wx, wy, op, border)
+            elif c % 3 == 1:
+                img = restatement.generate(w, h, 300 + c, dtype=dtype)
+                want = restatement.morph(img, wx, wy, op, border, bval)
+                halo = wy // 2
+                r0, r1 = h // 3, max(h // 3 + 1, 2 * h // 3)
+                a, z = max(0, r0 - halo), min(h, r1 + halo)
+                src = to_device(img[a:z], pad)
+                dst = empty_device((r1 - r0, w), dtype, pad)
+                gpu.morph_band_device(src, r0 - a, z - r1, dst, wx, wy, op, border, bval)
+                assert np.array_equal(to_host(dst), want[r0:r1]), ("band", knobs, c, w, h, wx, wy, op, border)
+            else:
+                img = restatement.generate(w, h, 600 + c, dtype=dtype)
+                got, _ = gpu_morph(gpu, img, wx, wy, op, border, bval, pad)
+                want = restatement.morph(img, wx, wy, op, border, bval)
+                assert np.array_equal(got, want), ("image", knobs, c, w, h, wx, wy, op, border)
+            seen.add(gpu.plan_name(es, w, h, wx, wy, op).split("_")[0])
+        assert "sep" in seen, seen
+    finally:
+        for k in SEP_KNOBS[knobs]:
+            gpu.debug_set(k, -1)
 
 
 def test_transpose_images(gpu, restatement):
