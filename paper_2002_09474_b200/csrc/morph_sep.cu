@@ -64,8 +64,9 @@ cudaError_t launch_v_t(const SepParams& p0, dim3 grid, cudaStream_t s, const Mor
     CUtensorMap lmap, tmap, omap;
     // the TMA pipeline pays off on large images (16384^2 u8 1x63: 77% vs 65% of HBM); on small ones
     // the plain-load kernel ramps faster (4096^2: 13.0 vs 15.4 us)
+    // (tall images only: a band touching the top or bottom border fills its rings synchronously)
     const long long px = (long long)j.W * j.H * j.batch;
-    const int no_tma = env_int("sep_notma", px >= (1LL << 26) ? 0 : 1);
+    const int no_tma = env_int("sep_notma", px >= (1LL << 26) && j.H >= 2048 ? 0 : 1);
     bool tma = !no_tma && stream::encode_input_map(j, SB / 4, B, &lmap) &&
                stream::encode_input_map(j, SB / 4, B + VRMAX, &tmap) && stream::encode_output_map(j, SB, B, &omap);
     if (tma) {
@@ -143,7 +144,7 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg) {
     int bands = (int)std::max(1LL, ((long long)sms * 24 * 32 + cols - 1) / cols);
     int rb = (j.H + bands - 1) / bands;
     rb = std::max(rb, 2 * (p.q - 1) * B);
-    if ((long long)j.W * j.H * j.batch >= (1LL << 26)) rb = std::max(rb, 320);  // TMA path: long bands
+    if ((long long)j.W * j.H * j.batch >= (1LL << 26) && j.H >= 2048) rb = std::max(rb, 320);  // TMA: long bands
     rb = env_int("sep_rb", rb);
     rb = std::max(B, (rb + B - 1) / B * B);
     p.rb = rb;
@@ -208,7 +209,7 @@ size_t scratch_pitch(const MorphJob& j) { return ((size_t)j.W * j.elem + 255) & 
 
 // Rows per L2 band of the intermediate (the whole image when it fits).
 int band_rows(const MorphJob& j) {
-    const size_t budget = (size_t)env_int("sep_l2mb", 40) << 20;
+    const size_t budget = (size_t)env_int("sep_l2mb", 1 << 12) << 20;  // measured: banded launches fill the GPU worse than one pass over the image
     const size_t per_row = scratch_pitch(j) * (size_t)j.batch;
     const long long rows = std::max<long long>(64, (long long)(budget / std::max<size_t>(per_row, 1)));
     return (int)std::min<long long>(rows, j.H);

@@ -530,31 +530,20 @@ __device__ __forceinline__ uint2 shdn(uint2 v, int d) {
     return make_uint2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
 }
 
-// One warp = one group of 4 rows; segments of 32 lane chunks; BX = g mod C (compile-time).
-// The next segment's rows are loaded before the current one is reduced (one segment in flight).
+// One warp item = 4 rows x one column part: segments of 32 lane chunks; BX = g mod C
+// (compile-time). The next segment's rows are loaded before the current one is reduced.
 template <typename T, int MODE, int C, int BX>
-__global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
+__device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0, size_t sp, uint8_t* drow0,
+                                       int nrows, int part) {
     using HC = HChunk<T, C>;
     constexpr int NW = HC::NW, sz = sizeof(T);
     const int lane = threadIdx.x & 31;
-    const int widx = blockIdx.x * (HT / 32) + (threadIdx.x >> 5);
-    const int gidx = widx / p.parts;
-    const int part = widx - gidx * p.parts;
-    const int img = gidx / p.groups;
-    const int grp = gidx - img * p.groups;
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // no-op unless launched as a PDL dependent
-    if (img >= p.batch) return;  // whole warp: no shuffle partner is left behind
     const int a = p.g / C;                   // whole chunks in the wing
     const int A = a + (BX > 0 ? 1 : 0);      // halo lanes on each side
     const int OS = (32 - 2 * A) * C;         // output columns per segment
     const int W = p.W;
-    const int y = grp * 4;
-    const int nrows = min(4, p.H - y);
-    const uint8_t* sb = p.src + (size_t)img * p.simg;
-    uint8_t* db = p.dst + (size_t)img * p.dimg;
-    const uint8_t* srow0 = sb + (size_t)y * p.sp;
-    // rows past H (last group) re-read row H-1; their results are never stored
-    const size_t rs1 = nrows > 1 ? p.sp : 0, rs2 = nrows > 2 ? 2 * p.sp : rs1, rs3 = nrows > 3 ? 3 * p.sp : rs2;
+    // rows past the last one re-read it; their results are never stored
+    const size_t rs1 = nrows > 1 ? sp : 0, rs2 = nrows > 2 ? 2 * sp : rs1, rs3 = nrows > 3 ? 3 * sp : rs2;
     const uint2 ID = ident2<MODE>();
 
     uint32_t r0[NW], r1[NW], r2[NW], r3[NW];
@@ -616,7 +605,7 @@ __global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
         uint32_t o0[NW], o1[NW], o2[NW], o3[NW];
         h_transpose_out<T, C>(o, o0, o1, o2, o3);
         if (lane >= A && lane < 32 - A && cx < W) {
-            uint8_t* drow = db + (size_t)y * p.dp + (ptrdiff_t)cx * sz;
+            uint8_t* drow = drow0 + (ptrdiff_t)cx * sz;
             if (cx + C <= W) {
                 h_store_row<T, C>(drow, o0);
                 if (nrows > 1) h_store_row<T, C>(drow + p.dp, o1);
@@ -624,15 +613,15 @@ __global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
                 if (nrows > 3) h_store_row<T, C>(drow + 3 * p.dp, o3);
             } else {
                 const int n = W - cx;
-                auto part = [&](int k, const uint32_t (&rw)[NW]) {
+                auto part_store = [&](int k, const uint32_t (&rw)[NW]) {
                     if (k < nrows)
                         for (int e = 0; e < n; ++e)
                             reinterpret_cast<T*>(drow + (size_t)k * p.dp)[e] = (T)(rw[(e * sz) / 4] >> ((e * sz * 8) & 31));
                 };
-                part(0, o0);
-                part(1, o1);
-                part(2, o2);
-                part(3, o3);
+                part_store(0, o0);
+                part_store(1, o1);
+                part_store(2, o2);
+                part_store(3, o3);
             }
         }
     }
@@ -646,8 +635,23 @@ __global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
         const int l1 = part == p.parts - 1 ? (W * sz + 127) / 128 : (ehi * sz) / 128;
         for (int k = 0; k < nrows; ++k)
             for (int l = l0 + lane; l < l1; l += 32)
-                asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(srow0 + (size_t)k * p.sp + (size_t)l * 128) : "memory");
+                asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(srow0 + (size_t)k * sp + (size_t)l * 128) : "memory");
     }
+}
+
+// One warp per (4-row group, column part).
+template <typename T, int MODE, int C, int BX>
+__global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
+    const int widx = blockIdx.x * (HT / 32) + (threadIdx.x >> 5);
+    const int gidx = widx / p.parts;
+    const int part = widx - gidx * p.parts;
+    const int img = gidx / p.groups;
+    const int grp = gidx - img * p.groups;
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // no-op unless launched as a PDL dependent
+    if (img >= p.batch) return;  // whole warp: no shuffle partner is left behind
+    const int y = grp * 4;
+    h_item<T, MODE, C, BX>(p, p.src + (size_t)img * p.simg + (size_t)y * p.sp, p.sp,
+                           p.dst + (size_t)img * p.dimg + (size_t)y * p.dp, min(4, p.H - y), part);
 }
 
 // H launch: after a V pass into the scratch band (p.discard) H is a programmatic dependent launch

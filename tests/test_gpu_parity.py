@@ -298,7 +298,8 @@ def test_sep_passes_fuzz(gpu, restatement, dtype, knobs):
     rng = np.random.default_rng(1234 + 7 * knobs + np.dtype(dtype).itemsize)
     mx = int(np.iinfo(dtype).max)
     es = np.dtype(dtype).itemsize
-    for k, v in SEP_KNOBS[knobs].items():
+    knob_set = dict(SEP_KNOBS[knobs], u16_phase_first=0)  # u16 goes to the phase kernel by default
+    for k, v in knob_set.items():
         gpu.debug_set(k, v)
     try:
         seen = set()
@@ -343,7 +344,7 @@ def test_sep_passes_fuzz(gpu, restatement, dtype, knobs):
             seen.add(gpu.plan_name(es, w, h, wx, wy, op).split("_")[0])
         assert "sep" in seen, seen
     finally:
-        for k in SEP_KNOBS[knobs]:
+        for k in knob_set:
             gpu.debug_set(k, -1)
 
 

@@ -19,7 +19,10 @@ tot = 0
 for r in rows[2:]:
     if len(r) <= E or not r[E]:
         continue
-    n = float(r[E])
+    try:
+        n = float(r[E])
+    except ValueError:  # header row of the next kernel in a multi-kernel report
+        continue
     src = r[ci["Source"]].strip()
     op = src.split()[0] if src else "?"
     if op.startswith("@"):
