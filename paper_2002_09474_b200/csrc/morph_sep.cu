@@ -18,7 +18,7 @@ cudaError_t launch_h_u16_max(const SepParams&, int C, int bx, dim3 grid, cudaStr
 
 namespace {
 
-constexpr int QM = 8;
+constexpr int QM = 4;  // block minima kept in registers (q - 1 <= QM)
 constexpr int kBlocks[] = {8, 10, 12, 14, 16, 18, 20, 22, 24};
 
 int env_int(const char* name, int dflt) { return tune(name, dflt); }
@@ -40,6 +40,11 @@ bool choose_b(int elem, int g, int* B_out) {
             bb = B;
         }
     }
+    const int forced = env_int("sep_vb", 0);  // tuning: force a block size when it is valid
+    if (forced > 0 && forced <= w1 && w1 % forced <= VRMAX && w1 / forced - 1 <= QM &&
+        (elem == 1 || forced <= 16))
+        for (int B : kBlocks)
+            if (B == forced) bb = B;
     *B_out = bb;
     return bb != 0;
 }

@@ -159,14 +159,22 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
     Raw xt[B], xl[B], xr[VRMAX];
     const int tb = base - w1;                    // first trailing row
     const int rb0 = base - (q - 1) * B - r;      // first of the r tail rows
+    auto load_lead = [&]() {
+        if constexpr (EDGE) {
+#pragma unroll
+            for (int m = 0; m < B; ++m) xl[m] = ldE(base + m);
+        } else {
+            const uint8_t* pl = s + (ptrdiff_t)base * sp;
+#pragma unroll
+            for (int m = 0; m < B; ++m) xl[m] = V::load(pl + m * sp);
+        }
+    };
     if constexpr (EDGE) {
 #pragma unroll
         for (int m = 0; m < B; ++m) xt[m] = ldE(tb + m);
 #pragma unroll
         for (int t = 0; t < VRMAX; ++t)
             if (t < r) xr[t] = ldE(rb0 + t);
-#pragma unroll
-        for (int m = 0; m < B; ++m) xl[m] = ldE(base + m);
     } else {
         const uint8_t* pt = s + (ptrdiff_t)tb * sp;
 #pragma unroll
@@ -175,10 +183,10 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
 #pragma unroll
         for (int t = 0; t < VRMAX; ++t)
             if (t < r) xr[t] = V::load(pr + t * sp);
-        const uint8_t* pl = s + (ptrdiff_t)base * sp;
-#pragma unroll
-        for (int m = 0; m < B; ++m) xl[m] = V::load(pl + m * sp);
     }
+#ifndef SEP_VSPLIT
+    load_lead();  // all 2B (+r) loads in flight before the first reduction
+#endif
     uint2 Tm[B];
     uint2 acc = V::unpack(xt[B - 1]);
     Tm[B - 1] = acc;
@@ -192,6 +200,10 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
     for (int t = 0; t < VRMAX; ++t) G = op2<MODE>(G, t < r ? V::unpack(xr[t]) : ID);
 #pragma unroll
     for (int k = 0; k + 1 < QM; k += 2) G = op3<MODE>(G, k < q - 1 ? M[k] : ID, k + 1 < q - 1 ? M[k + 1] : ID);
+#ifdef SEP_VSPLIT
+    asm volatile("" ::: "memory");  // leading loads after the trailing suffix: B fewer live registers
+    load_lead();
+#endif
     uint2 P = ID;
 #pragma unroll
     for (int m = 0; m < B; ++m) {
@@ -249,8 +261,17 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
     }
 }
 
+// Measured (4096^2 / 16384^2 u8 1x63): 4 resident CTAs (<= 128 registers, small spills on the
+// border path) with the leading loads issued after the trailing suffix beat 3 CTAs with every load
+// hoisted: 12.4 vs 13-16 us, 65.5% vs 52-62% of HBM.
+#ifndef SEP_VMINB
+#define SEP_VMINB 4
+#endif
+#ifndef SEP_VHOIST
+#define SEP_VSPLIT 1
+#endif
 template <typename T, int MODE, int B, int QM>
-__global__ void __launch_bounds__(VT) vpass_kernel(const SepParams p) {
+__global__ void __launch_bounds__(VT, SEP_VMINB) vpass_kernel(const SepParams p) {
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // H may start scheduling
     const int c = blockIdx.x * VT + threadIdx.x;
     if (c >= p.nwords) return;
