@@ -148,7 +148,8 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg) {
     const int sms = device_sm_count();
     int bands = (int)std::max(1LL, ((long long)sms * 24 * 32 + cols - 1) / cols);
     int rb = (j.H + bands - 1) / bands;
-    rb = std::max(rb, 2 * (p.q - 1) * B);
+    // no floor for the warm-up (q-1 blocks per band): cfg2 measured best with ~24 warps/SM even
+    // when the warm-up is 2x a band (4096^2 101x101: 25.5 vs 28.2 us at the old 2(q-1)B floor)
     if ((long long)j.W * j.H * j.batch >= (1LL << 26) && j.H >= 2048) rb = std::max(rb, 320);  // TMA: long bands
     rb = env_int("sep_rb", rb);
     rb = std::max(B, (rb + B - 1) / B * B);
