@@ -150,7 +150,9 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg) {
     int rb = (j.H + bands - 1) / bands;
     // no floor for the warm-up (q-1 blocks per band): cfg2 measured best with ~24 warps/SM even
     // when the warm-up is 2x a band (4096^2 101x101: 25.5 vs 28.2 us at the old 2(q-1)B floor)
-    if ((long long)j.W * j.H * j.batch >= (1LL << 26) && j.H >= 2048) rb = std::max(rb, 320);  // TMA: long bands
+    // TMA path: bands of 320-640 rows (32768^2 63x63: rb 640 865 us, 160 895 us, one band per warp
+    // per 2341 rows 1081 us)
+    if ((long long)j.W * j.H * j.batch >= (1LL << 26) && j.H >= 2048) rb = std::min(std::max(rb, 320), 640);
     rb = env_int("sep_rb", rb);
     rb = std::max(B, (rb + B - 1) / B * B);
     p.rb = rb;
@@ -237,7 +239,9 @@ cudaError_t run(const MorphJob& j, void* tmp) {
         b.below = j.below + (j.H - y0 - rows);
         cudaError_t e = run_v(b, tmp, tp, timg);
         if (e != cudaSuccess) return e;
-        e = run_h(b, tmp, tp, timg, 1);
+        // discard the intermediate's lines only when the band can still be in L2 (measured: on a
+        // 1 GiB intermediate the discards cost 7%)
+        e = run_h(b, tmp, tp, timg, env_int("sep_discard", timg * b.batch <= (size_t)64 << 20 ? 1 : 0));
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

@@ -166,7 +166,10 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
         } else {
             const uint8_t* pl = s + (ptrdiff_t)base * sp;
 #pragma unroll
-            for (int m = 0; m < B; ++m) xl[m] = V::load(pl + m * sp);
+            for (int m = 0; m < B; ++m) {  // pointer bumps: one 64-bit add per row
+                xl[m] = V::load(pl);
+                pl += sp;
+            }
         }
     };
     if constexpr (EDGE) {
@@ -178,11 +181,16 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
     } else {
         const uint8_t* pt = s + (ptrdiff_t)tb * sp;
 #pragma unroll
-        for (int m = 0; m < B; ++m) xt[m] = V::load(pt + m * sp);
-        const uint8_t* pr = s + (ptrdiff_t)rb0 * sp;
+        for (int m = 0; m < B; ++m) {
+            xt[m] = V::load(pt);
+            pt += sp;
+        }
+        // the r tail rows follow the trailing batch directly (rb0 = tb + B)
 #pragma unroll
-        for (int t = 0; t < VRMAX; ++t)
-            if (t < r) xr[t] = V::load(pr + t * sp);
+        for (int t = 0; t < VRMAX; ++t) {
+            if (t < r) xr[t] = V::load(pt);
+            pt += sp;
+        }
     }
 #ifndef SEP_VSPLIT
     load_lead();  // all 2B (+r) loads in flight before the first reduction
@@ -205,17 +213,18 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
     load_lead();
 #endif
     uint2 P = ID;
+    uint8_t* d = drow;
 #pragma unroll
     for (int m = 0; m < B; ++m) {
         P = op2<MODE>(P, V::unpack(xl[m]));
         const uint2 o = op3<MODE>(Tm[m], G, P);
-        uint8_t* d = drow + (ptrdiff_t)m * (ptrdiff_t)p.dp;
         if constexpr (FULL) {
             W4<T>::store(d, o);
         } else if (m < nst) {
             if (nvalid == 4) W4<T>::store(d, o);
             else store_partial<T>(d, o, nvalid);
         }
+        d += p.dp;
     }
 #pragma unroll
     for (int k = QM - 1; k > 0; --k) M[k] = M[k - 1];
@@ -235,14 +244,16 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
     for (int L = -(p.q - 1); L < 0; ++L) {
         const int base = i0 + L * B;
         typename V::Raw x[B];
+        const uint8_t* pw = s + (ptrdiff_t)base * (ptrdiff_t)p.sp;
 #pragma unroll
         for (int m = 0; m < B; ++m) {
-            int i = base + m;
             if constexpr (EDGE) {
+                const int i = base + m;
                 const int ic = min(max(i, p.row_lo), p.row_hi - 1);
                 x[m] = V::sel(p.cmode && ic != i, V::splat(p.bval), V::load(s + (ptrdiff_t)ic * (ptrdiff_t)p.sp));
             } else {
-                x[m] = V::load(s + (ptrdiff_t)i * (ptrdiff_t)p.sp);
+                x[m] = V::load(pw);
+                pw += p.sp;
             }
         }
         uint2 P = V::unpack(x[0]);
