@@ -230,9 +230,9 @@ int run_single(MorphJob j) {
         if (e != cudaSuccess) return cuda_fail(e, "register-streaming morph kernel");
         return RMGPU_OK;
     }
-    // u16 (cfg4's batches of 1024^2 images): the phase kernel measured faster than the two passes
-    // (21x21 opening x512: 1923 vs 2040 us); sep takes what it declines
-    if (!g_disable_stream && j.elem == 2 && rmgpu::tune("u16_phase_first", 1) && rmgpu::phase::launch(j, &e)) {
+    // tuning knob: u16 through the phase kernel first (cfg4, 21x21 opening x512: K3 1719 us vs K2
+    // 1921 us, so K3 is the default)
+    if (!g_disable_stream && j.elem == 2 && rmgpu::tune("u16_phase_first", 0) && rmgpu::phase::launch(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "phase morph kernel");
         return RMGPU_OK;
     }
@@ -506,7 +506,7 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
     if (j.gx == 0 && j.gy == 0) return "copy";
     if (!g_disable_stream)
         if (const char* n = rmgpu::col::plan_name(j)) return n;
-    if (!g_disable_stream && j.elem == 2 && rmgpu::tune("u16_phase_first", 1))
+    if (!g_disable_stream && j.elem == 2 && rmgpu::tune("u16_phase_first", 0))
         if (const char* n = rmgpu::phase::plan_name(j)) return n;
     if (!g_disable_stream)
         if (const char* n = rmgpu::sep::plan_name(j)) return n;

@@ -288,6 +288,31 @@ SEP_KNOBS = [
 ]
 
 
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_phase_kernel_fuzz(gpu, restatement, dtype):
+    # K2 (persistent phase kernel) with K3 switched off: it stays the path for windows K3 declines
+    # (one wing in 1..3 with the other large, wings past K3's register budget) and must stay exact
+    rng = np.random.default_rng(77 + np.dtype(dtype).itemsize)
+    mx = int(np.iinfo(dtype).max)
+    es = np.dtype(dtype).itemsize
+    gpu.debug_set("sep", 0)
+    try:
+        seen = set()
+        for c in range(40):
+            w, h = int(rng.integers(1, 700)), int(rng.integers(1, 300))
+            wx = 2 * int(rng.integers(0, 50)) + 1
+            wy = 2 * int(rng.integers(4, 50)) + 1 if c % 2 else 2 * int(rng.integers(0, 4)) + 1
+            op, border, bval = int(rng.integers(0, 2)), int(rng.integers(0, 2)), int(rng.integers(0, mx + 1))
+            pad = (-w) % (16 // es)
+            img = restatement.generate(w, h, 40 + c, dtype=dtype)
+            got, _ = gpu_morph(gpu, img, wx, wy, op, border, bval, pad)
+            assert np.array_equal(got, restatement.morph(img, wx, wy, op, border, bval)), (c, w, h, wx, wy, op, border)
+            seen.add(gpu.plan_name(es, w, h, wx, wy, op).split("_")[0])
+        assert "phase" in seen, seen
+    finally:
+        gpu.debug_set("sep", -1)
+
+
 @pytest.mark.parametrize("knobs", range(len(SEP_KNOBS)))
 @pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
 def test_sep_passes_fuzz(gpu, restatement, dtype, knobs):
@@ -298,7 +323,7 @@ def test_sep_passes_fuzz(gpu, restatement, dtype, knobs):
     rng = np.random.default_rng(1234 + 7 * knobs + np.dtype(dtype).itemsize)
     mx = int(np.iinfo(dtype).max)
     es = np.dtype(dtype).itemsize
-    knob_set = dict(SEP_KNOBS[knobs], u16_phase_first=0)  # u16 goes to the phase kernel by default
+    knob_set = dict(SEP_KNOBS[knobs])
     for k, v in knob_set.items():
         gpu.debug_set(k, v)
     try:
