@@ -251,21 +251,43 @@ int run_single(MorphJob j) {
         return RMGPU_OK;
     }
     if (j.mode == rmgpu::MODE_GRAD && !g_disable_stream) {
-        // large-window gradient: dilation into scratch and erosion into dst with the phase kernel,
-        // then dst = dilation - erosion (dispatch.cpp:58-71; never negative, no wrap)
+        // large-window gradient: dilation into scratch and erosion into dst (K3, else the phase
+        // kernel), then dst = dilation - erosion (dispatch.cpp:58-71; never negative, no wrap)
+        auto minmax = [&](const MorphJob& m, int* rc) -> bool {  // false: neither kernel takes it
+            if (rmgpu::sep::applicable(m)) {
+                const size_t tb = rmgpu::sep::scratch_bytes(m);
+                void* tmp = nullptr;
+                cudaError_t ae = tb ? scratch_alloc(&tmp, tb, m.stream) : cudaSuccess;
+                if (ae != cudaSuccess) {
+                    *rc = cuda_fail(ae, "scratch");
+                    return true;
+                }
+                cudaError_t re = rmgpu::sep::run(m, tmp);
+                cudaError_t fe = tb ? cudaFreeAsync(tmp, m.stream) : cudaSuccess;
+                if (re != cudaSuccess) *rc = cuda_fail(re, "separable streaming passes (gradient)");
+                else if (fe != cudaSuccess) *rc = cuda_fail(fe, "cudaFreeAsync");
+                return true;
+            }
+            cudaError_t pe = cudaSuccess;
+            if (!rmgpu::phase::launch(m, &pe)) return false;
+            if (pe != cudaSuccess) *rc = cuda_fail(pe, "phase morph kernel (gradient)");
+            return true;
+        };
         const size_t rb = (size_t)j.W * j.elem, tp = (rb + 255) & ~size_t(255), timg = tp * (size_t)j.H;
-        void* hi = nullptr;
-        RM_CUDA(scratch_alloc(&hi, timg * j.batch, j.stream));
-        MorphJob mx = j;
+        MorphJob mx = j, mn = j;
         mx.mode = rmgpu::MODE_MAX;
-        mx.dst = hi; mx.dp = tp; mx.dimg = timg;
-        int rc = RMGPU_OK;
-        if (rmgpu::phase::launch(mx, &e)) {
-            if (e != cudaSuccess) rc = cuda_fail(e, "phase morph kernel (gradient, dilation)");
-            MorphJob mn = j;
-            mn.mode = rmgpu::MODE_MIN;
-            if (rc == RMGPU_OK && (!rmgpu::phase::launch(mn, &e) || e != cudaSuccess))
-                rc = cuda_fail(e != cudaSuccess ? e : cudaErrorInvalidValue, "phase morph kernel (gradient, erosion)");
+        mn.mode = rmgpu::MODE_MIN;
+        {
+            void* hi = nullptr;
+            RM_CUDA(scratch_alloc(&hi, timg * j.batch, j.stream));
+            mx.dst = hi; mx.dp = tp; mx.dimg = timg;
+            // K3 needs 16-byte aligned pitches on both sides: the scratch has them; when dst does not,
+            // sep::applicable(mn) is false and the phase kernel (or the fallbacks below) take over
+            int rc = RMGPU_OK;
+            if (!minmax(mx, &rc) || (rc == RMGPU_OK && !minmax(mn, &rc))) {
+                cudaFreeAsync(hi, j.stream);  // neither kernel takes this shape: the fallbacks below do
+                goto gradient_fallback;
+            }
             for (int b = 0; rc == RMGPU_OK && b < j.batch; ++b) {
                 char* d = static_cast<char*>(j.dst) + b * j.dimg;
                 e = rmgpu::launch_subtract(static_cast<char*>(hi) + b * timg, tp, d, j.dp, d, j.dp, j.W, j.H, j.elem,
@@ -276,8 +298,8 @@ int run_single(MorphJob j) {
             if (rc == RMGPU_OK && fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
             return rc;
         }
-        cudaFreeAsync(hi, j.stream);
     }
+gradient_fallback:
     if (rmgpu::launch_fast(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "fast morph kernel");
         return RMGPU_OK;
@@ -515,7 +537,9 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
     if (j.mode == rmgpu::MODE_GRAD && !g_disable_stream) {
         MorphJob m = j;
         m.mode = rmgpu::MODE_MAX;
-        if (const char* n = rmgpu::phase::plan_name(m)) {
+        const char* n = rmgpu::sep::plan_name(m);
+        if (!n) n = rmgpu::phase::plan_name(m);
+        if (n) {
             static thread_local std::string g;
             g = std::string("gradient[2x ") + n + " + subtract]";
             return g.c_str();
