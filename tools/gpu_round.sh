@@ -17,5 +17,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --c
   --soak-seconds 0 > gpurun_out/ncu_launch.log 2>&1
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:morph_col -s 8 -c 1 \
   -o gpurun_out/col3 -f python tools/time_morph.py 4096 4096 3 3 0 1 --nograph > gpurun_out/ncu_col.log 2>&1
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:morph_phase -s 4 -c 1 \
-  -o gpurun_out/phase63 -f python tools/time_morph.py 4096 4096 63 63 0 1 --nograph > gpurun_out/ncu_phase.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:"pass_kernel|vtma" -s 4 -c 2 \
+  -o gpurun_out/sep63 -f python tools/time_morph.py 4096 4096 63 63 0 1 --nograph > gpurun_out/ncu_sep.log 2>&1
