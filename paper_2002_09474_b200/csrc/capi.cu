@@ -382,6 +382,19 @@ int run_morph(const void* src, size_t sp, size_t simg, void* dst, size_t dp, siz
         j.mode = op == RMGPU_ERODE ? rmgpu::MODE_MIN : op == RMGPU_DILATE ? rmgpu::MODE_MAX : rmgpu::MODE_GRAD;
         return run_single(j);
     }
+    if (!g_disable_stream && above == 0 && below == 0) {
+        MorphJob c = j;
+        c.mode = op == RMGPU_OPEN ? rmgpu::MODE_MIN : rmgpu::MODE_MAX;
+        if (rmgpu::sep::compound_applicable(c)) {
+            void* tmp = nullptr;
+            RM_CUDA(scratch_alloc(&tmp, rmgpu::sep::compound_scratch_bytes(c), stream));
+            cudaError_t ce = rmgpu::sep::run_compound(c, tmp);
+            cudaError_t fe = cudaFreeAsync(tmp, stream);
+            if (ce != cudaSuccess) return cuda_fail(ce, "opening/closing (K3, fused horizontal passes)");
+            if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
+            return RMGPU_OK;
+        }
+    }
     // opening = dilate(erode(x)), closing = erode(dilate(x)) (dispatch.cpp:48-56): the first stage
     // runs over the band plus up to one wing of halo rows, its result is a real image whose border
     // (the true image border) is re-applied by the second stage.

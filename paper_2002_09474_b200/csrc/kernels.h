@@ -73,6 +73,10 @@ bool applicable(const MorphJob& j);
 size_t scratch_bytes(const MorphJob& j);  // 0: no intermediate (one axis has window 1)
 cudaError_t run(const MorphJob& j, void* tmp);
 const char* plan_name(const MorphJob& j);
+// opening (mode MIN first) / closing (MAX first) in three launches; whole images only
+bool compound_applicable(const MorphJob& j);
+size_t compound_scratch_bytes(const MorphJob& j);
+cudaError_t run_compound(const MorphJob& j, void* tmp);
 }  // namespace sep
 
 // ---- transposes (transpose.cu) ---------------------------------------------------------------

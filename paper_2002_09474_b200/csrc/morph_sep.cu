@@ -15,6 +15,10 @@ cudaError_t launch_h_u8_min(const SepParams&, int C, int bx, dim3 grid, cudaStre
 cudaError_t launch_h_u8_max(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
 cudaError_t launch_h_u16_min(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
 cudaError_t launch_h_u16_max(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
+cudaError_t launch_hh_u8_min(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
+cudaError_t launch_hh_u8_max(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
+cudaError_t launch_hh_u16_min(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
+cudaError_t launch_hh_u16_max(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
 
 namespace {
 
@@ -164,8 +168,9 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg) {
     return launch_v(p, j.elem, j.mode, B, grid, j.stream, jo);
 }
 
-// One horizontal pass over H rows: in -> job dst.
-cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int discard) {
+// One horizontal pass over H rows: in -> job dst (stages = 2: this mode then the other, the two
+// horizontal passes of an opening / closing).
+cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int discard, int stages = 1) {
     int C = 0;
     if (!choose_c(j.elem, j.gx, &C)) return cudaErrorInvalidValue;
     SepParams p = base_params(j);
@@ -179,8 +184,9 @@ cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int
     p.groups = (j.H + 3) / 4;
     p.discard = discard;
     // parts: ~24 resident warps per SM, each part a whole number of segments
-    const int A = j.gx / C + (j.gx % C ? 1 : 0);
+    const int A = stages * (j.gx / C + (j.gx % C ? 1 : 0));
     const int OS = (32 - 2 * A) * C;
+    if (OS <= 0) return cudaErrorInvalidValue;
     const int nseg = (j.W + OS - 1) / OS;
     const long long rowsw = (long long)p.groups * j.batch;
     // each warp keeps one segment in flight: parts of <= 8 segments (measured: 4096^2 u8 63x1 best
@@ -192,6 +198,11 @@ cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int
     p.parts = (nseg + segs_per - 1) / segs_per;
     const long long warps = rowsw * p.parts;
     const dim3 grid((unsigned)((warps + HT / 32 - 1) / (HT / 32)));
+    if (stages == 2) {
+        const int bx = p.g % C;
+        if (j.elem == 1) return j.mode == MODE_MIN ? launch_hh_u8_min(p, C, bx, grid, j.stream) : launch_hh_u8_max(p, C, bx, grid, j.stream);
+        return j.mode == MODE_MIN ? launch_hh_u16_min(p, C, bx, grid, j.stream) : launch_hh_u16_max(p, C, bx, grid, j.stream);
+    }
     return launch_h(p, j.elem, j.mode, C, grid, j.stream);
 }
 
@@ -211,6 +222,43 @@ bool applicable(const MorphJob& j) {
     if (j.gy != 0 && !choose_b(j.elem, j.gy, &t)) return false;
     if (j.gx != 0 && !choose_c(j.elem, j.gx, &t)) return false;
     return true;
+}
+
+// Opening (j.mode = MODE_MIN first) / closing (MODE_MAX first) of whole images (no halo rows) in
+// three launches instead of four: opening = Dv o (Dh o Eh) o Ev -- each separable op may run its
+// passes in either order, so the two horizontal passes meet in the middle and run as one sweep
+// (the intermediate between them never leaves registers; its column border is re-applied there).
+bool compound_applicable(const MorphJob& j) {
+    if (!applicable(j) || j.above || j.below || j.gx == 0 || j.gy == 0) return false;
+    if (!env_int("sep_hh", 1)) return false;
+    int C = 0;
+    choose_c(j.elem, j.gx, &C);
+    const int A = j.gx / C + (j.gx % C ? 1 : 0);
+    return 2 * A <= 10;  // the left border fix needs the second segment clear of negative columns
+}
+
+size_t compound_scratch_bytes(const MorphJob& j) {
+    return 2 * (((size_t)j.W * j.elem + 255) & ~size_t(255)) * (size_t)j.H * (size_t)j.batch;
+}
+
+cudaError_t run_compound(const MorphJob& j, void* tmp) {
+    const size_t tp = ((size_t)j.W * j.elem + 255) & ~size_t(255), timg = tp * (size_t)j.H;
+    uint8_t* t1 = static_cast<uint8_t*>(tmp);
+    uint8_t* t2 = t1 + timg * (size_t)j.batch;
+    const int second = j.mode == MODE_MIN ? MODE_MAX : MODE_MIN;
+    cudaError_t e = run_v(j, t1, tp, timg);  // first op, vertical
+    if (e != cudaSuccess) return e;
+    MorphJob h = j;  // first op horizontal, then second op horizontal: t1 -> t2
+    h.dst = t2;
+    h.dp = tp;
+    h.dimg = timg;
+    if ((e = run_h(h, t1, tp, timg, 1, 2)) != cudaSuccess) return e;
+    MorphJob v = j;  // second op, vertical: t2 -> dst (rows outside the image: the image border)
+    v.mode = second;
+    v.src = t2;
+    v.sp = tp;
+    v.simg = timg;
+    return run_v(v, j.dst, j.dp, j.dimg);
 }
 
 size_t scratch_pitch(const MorphJob& j) { return ((size_t)j.W * j.elem + 255) & ~size_t(255); }

@@ -564,23 +564,96 @@ __device__ __forceinline__ uint2 shdn(uint2 v, int d) {
 
 // One warp item = 4 rows x one column part: segments of 32 lane chunks; BX = g mod C
 // (compile-time). The next segment's rows are loaded before the current one is reduced.
-template <typename T, int MODE, int C, int BX>
+// One lane-chunk van Herk pass over the columns of a segment: x = this lane's C columns (4 rows
+// each), o = the window result for those columns (valid where the window's chunks are loaded).
+template <int MODE, int C, int BX>
+__device__ __forceinline__ void h_lane_pass(const uint2 (&x)[C], int a, uint2 (&o)[C]) {
+    const uint2 ID = ident2<MODE>();
+    uint2 P[C], S[C];
+    P[0] = x[0];
+#pragma unroll
+    for (int c = 1; c < C; ++c) P[c] = op2<MODE>(P[c - 1], x[c]);
+    S[C - 1] = x[C - 1];
+#pragma unroll
+    for (int c = C - 2; c >= 0; --c) S[c] = op2<MODE>(S[c + 1], x[c]);
+    const uint2 cm = P[C - 1];
+    // chunk minima strictly inside the window: lanes L-a+1 .. L+a-1, plus lane L-a when the
+    // left end lies one chunk further out (dl) and lane L+a when the right end does (dr)
+    uint2 base = a > 0 ? cm : ID;
+    for (int dd = 1; dd < a; ++dd) base = op3<MODE>(base, shup(cm, dd), shdn(cm, dd));
+    const uint2 ml = shup(cm, a), mr = shdn(cm, a);
+    uint2 m00 = base, m10, m01, m11;
+    if (a > 0) {
+        m10 = op2<MODE>(base, ml);
+        m01 = op2<MODE>(base, mr);
+        m11 = op3<MODE>(base, ml, mr);
+    } else {  // a = 0: only both ends one chunk out leave a whole chunk (this lane's) inside
+        m10 = ID;
+        m01 = ID;
+        m11 = cm;
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+        const bool dl = j < BX;       // left end in chunk L-a-1
+        const bool dr = j + BX >= C;  // right end in chunk L+a+1
+        const uint2 sl = shup(S[(j - BX + C) % C], a + (dl ? 1 : 0));
+        const uint2 pr = shdn(P[(j + BX) % C], a + (dr ? 1 : 0));
+        const uint2 mid = dl ? (dr ? m11 : m10) : (dr ? m01 : m00);
+        o[j] = op3<MODE>(sl, mid, pr);
+    }
+}
+
+// The border of the intermediate image between the two horizontal passes of an opening/closing:
+// columns outside [0, W) take the constant, or (replicate) the intermediate's column 0 / W-1.
+template <typename T, int C>
+__device__ __forceinline__ void h_border_fix(uint2 (&o)[C], int X, int cx, int HA, int W, int cmode, uint32_t bval) {
+    const int lane = threadIdx.x & 31;
+    const bool left = X < HA * C, right = X + (32 - HA) * C > W;  // warp-uniform
+    if (!left && !right) return;
+    uint2 lv, rv;
+    if (cmode) {
+        const uint32_t w = sizeof(T) == 1 ? bval * 0x01010101u : bval * 0x00010001u;
+        lv = rv = make_uint2(w, w);
+    } else {
+        lv = make_uint2(__shfl_sync(0xffffffffu, o[0].x, min(31, max(0, HA - X / C))),
+                        __shfl_sync(0xffffffffu, o[0].y, min(31, max(0, HA - X / C))));
+        const int lw = min(31, max(0, HA + (W - 1 - X) / C)), pw = (W - 1 - X) % C;
+        uint2 mine = o[0];
+#pragma unroll
+        for (int j = 1; j < C; ++j)
+            if (j == pw) mine = o[j];
+        rv = make_uint2(__shfl_sync(0xffffffffu, mine.x, lw), __shfl_sync(0xffffffffu, mine.y, lw));
+    }
+    (void)lane;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+        if (cx + j < 0) o[j] = lv;
+        else if (cx + j >= W) o[j] = rv;
+    }
+}
+
+// One warp item = 4 rows x one column part: segments of 32 lane chunks; BX = g mod C
+// (compile-time). The next segment's rows are loaded before the current one is reduced.
+// STAGES = 2: the two horizontal passes of an opening (MODE = min, then max) or closing in one
+// sweep -- the first pass's result never leaves registers; halo lanes double.
+template <typename T, int MODE, int C, int BX, int STAGES = 1>
 __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0, size_t sp, uint8_t* drow0,
                                        int nrows, int part) {
     using HC = HChunk<T, C>;
     constexpr int NW = HC::NW, sz = sizeof(T);
+    constexpr int MODE2 = MODE == MODE_MIN ? MODE_MAX : MODE_MIN;
     const int lane = threadIdx.x & 31;
     const int a = p.g / C;                   // whole chunks in the wing
-    const int A = a + (BX > 0 ? 1 : 0);      // halo lanes on each side
-    const int OS = (32 - 2 * A) * C;         // output columns per segment
+    const int A = a + (BX > 0 ? 1 : 0);      // halo lanes on each side, per pass
+    const int HA = STAGES * A;
+    const int OS = (32 - 2 * HA) * C;        // output columns per segment
     const int W = p.W;
     // rows past the last one re-read it; their results are never stored
     const size_t rs1 = nrows > 1 ? sp : 0, rs2 = nrows > 2 ? 2 * sp : rs1, rs3 = nrows > 3 ? 3 * sp : rs2;
-    const uint2 ID = ident2<MODE>();
 
     uint32_t r0[NW], r1[NW], r2[NW], r3[NW];
     auto load_seg = [&](int X) {
-        const int cx = X + (lane - A) * C;
+        const int cx = X + (lane - HA) * C;
         if (cx >= 0 && cx + C <= W) {
             const uint8_t* b = srow0 + (ptrdiff_t)cx * sz;
             h_load_row<T, C>(b, r0);
@@ -597,46 +670,21 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
     const int xlo = part * p.pw, xhi = min(W, xlo + p.pw);
     load_seg(xlo);
     for (int X = xlo; X < xhi; X += OS) {
-        const int cx = X + (lane - A) * C;  // first column of this lane's chunk
+        const int cx = X + (lane - HA) * C;  // first column of this lane's chunk
         uint2 x[C];
         h_transpose_in<T, C>(r0, r1, r2, r3, x);
         if (X + OS < xhi) load_seg(X + OS);
-        uint2 P[C], S[C];
-        P[0] = x[0];
-#pragma unroll
-        for (int c = 1; c < C; ++c) P[c] = op2<MODE>(P[c - 1], x[c]);
-        S[C - 1] = x[C - 1];
-#pragma unroll
-        for (int c = C - 2; c >= 0; --c) S[c] = op2<MODE>(S[c + 1], x[c]);
-        const uint2 cm = P[C - 1];
-        // chunk minima strictly inside the window: lanes L-a+1 .. L+a-1, plus lane L-a when the
-        // left end lies one chunk further out (dl) and lane L+a when the right end does (dr)
-        uint2 base = a > 0 ? cm : ID;
-        for (int dd = 1; dd < a; ++dd) base = op3<MODE>(base, shup(cm, dd), shdn(cm, dd));
-        const uint2 ml = shup(cm, a), mr = shdn(cm, a);
-        uint2 m00 = base, m10, m01, m11;
-        if (a > 0) {
-            m10 = op2<MODE>(base, ml);
-            m01 = op2<MODE>(base, mr);
-            m11 = op3<MODE>(base, ml, mr);
-        } else {  // a = 0: only both ends one chunk out leave a whole chunk (this lane's) inside
-            m10 = ID;
-            m01 = ID;
-            m11 = cm;
-        }
         uint2 o[C];
+        h_lane_pass<MODE, C, BX>(x, a, o);
+        if constexpr (STAGES == 2) {
+            h_border_fix<T, C>(o, X, cx, HA, W, p.cmode, p.bval);
+            h_lane_pass<MODE2, C, BX>(o, a, x);
 #pragma unroll
-        for (int j = 0; j < C; ++j) {
-            const bool dl = j < BX;       // left end in chunk L-a-1
-            const bool dr = j + BX >= C;  // right end in chunk L+a+1
-            const uint2 sl = shup(S[(j - BX + C) % C], a + (dl ? 1 : 0));
-            const uint2 pr = shdn(P[(j + BX) % C], a + (dr ? 1 : 0));
-            const uint2 mid = dl ? (dr ? m11 : m10) : (dr ? m01 : m00);
-            o[j] = op3<MODE>(sl, mid, pr);
+            for (int k = 0; k < C; ++k) o[k] = x[k];
         }
         uint32_t o0[NW], o1[NW], o2[NW], o3[NW];
         h_transpose_out<T, C>(o, o0, o1, o2, o3);
-        if (lane >= A && lane < 32 - A && cx < W) {
+        if (lane >= HA && lane < 32 - HA && cx < W) {
             uint8_t* drow = drow0 + (ptrdiff_t)cx * sz;
             if (cx + C <= W) {
                 h_store_row<T, C>(drow, o0);
@@ -661,8 +709,8 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
         // drop the source lines only this warp reads (its part minus the halos the neighbouring
         // parts read) from L2 unwritten: the source is a private scratch band
         __syncwarp();
-        const int elo = part == 0 ? 0 : xlo + A * C;
-        const int ehi = part == p.parts - 1 ? W : xhi - A * C;
+        const int elo = part == 0 ? 0 : xlo + HA * C;
+        const int ehi = part == p.parts - 1 ? W : xhi - HA * C;
         const int l0 = part == 0 ? 0 : (elo * sz + 127) / 128;
         const int l1 = part == p.parts - 1 ? (W * sz + 127) / 128 : (ehi * sz) / 128;
         for (int k = 0; k < nrows; ++k)
@@ -672,7 +720,7 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
 }
 
 // One warp per (4-row group, column part).
-template <typename T, int MODE, int C, int BX>
+template <typename T, int MODE, int C, int BX, int STAGES = 1>
 __global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
     const int widx = blockIdx.x * (HT / 32) + (threadIdx.x >> 5);
     const int gidx = widx / p.parts;
@@ -682,7 +730,7 @@ __global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // no-op unless launched as a PDL dependent
     if (img >= p.batch) return;  // whole warp: no shuffle partner is left behind
     const int y = grp * 4;
-    h_item<T, MODE, C, BX>(p, p.src + (size_t)img * p.simg + (size_t)y * p.sp, p.sp,
+    h_item<T, MODE, C, BX, STAGES>(p, p.src + (size_t)img * p.simg + (size_t)y * p.sp, p.sp,
                            p.dst + (size_t)img * p.dimg + (size_t)y * p.dp, min(4, p.H - y), part);
 }
 

@@ -336,7 +336,7 @@ def test_sep_passes_fuzz(gpu, restatement, dtype, knobs):
             wy = 2 * g[int(rng.integers(0, 3))] + 1 if c % 5 else 1
             if wx == 1 and wy == 1:
                 wx = 2 * int(rng.integers(4, 40)) + 1
-            op = int(rng.integers(0, 2))
+            op = int(rng.integers(0, 5))  # erode, dilate, opening, closing, gradient
             border = int(rng.integers(0, 2))
             bval = int(rng.integers(0, mx + 1))
             pad = (-w) % (16 // es) + 16 // es * int(rng.integers(0, 3))
@@ -354,7 +354,7 @@ def test_sep_passes_fuzz(gpu, restatement, dtype, knobs):
             elif c % 3 == 1:
                 img = restatement.generate(w, h, 300 + c, dtype=dtype)
                 want = restatement.morph(img, wx, wy, op, border, bval)
-                halo = wy // 2
+                halo = (wy // 2) * (2 if op in (OPEN, CLOSE) else 1)
                 r0, r1 = h // 3, max(h // 3 + 1, 2 * h // 3)
                 a, z = max(0, r0 - halo), min(h, r1 + halo)
                 src = to_device(img[a:z], pad)
