@@ -90,9 +90,11 @@ cudaError_t launch_v_t(const SepParams& p0, dim3 grid, cudaStream_t s, const Mor
         const int smem = VTW * p.wsmem;
         kernel_occupancy((const void*)kern, VT, smem, &e);
         if (e != cudaSuccess) return e;
-        kern<<<dim3((unsigned)((warps + VTW - 1) / VTW)), VT, smem, s>>>(p, lmap, tmap, omap);
+        cudaError_t le = launch_pdl(kern, dim3((unsigned)((warps + VTW - 1) / VTW)), dim3(VT), smem, s, p, lmap, tmap, omap);
+        if (le != cudaSuccess) return le;
     } else {
-        vpass_kernel<T, MODE, B, QM><<<grid, VT, 0, s>>>(p);
+        cudaError_t le = launch_pdl(vpass_kernel<T, MODE, B, QM>, grid, dim3(VT), 0, s, p);
+        if (le != cudaSuccess) return le;
     }
     count_launch();
     return cudaGetLastError();
@@ -131,7 +133,7 @@ SepParams base_params(const MorphJob& j) {
 }
 
 // One vertical pass over the job's rows: src (rows [-above, H + below) valid) -> out.
-cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg) {
+cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl = 0) {
     int B = 0;
     if (!choose_b(j.elem, j.gy, &B)) return cudaErrorInvalidValue;
     SepParams p = base_params(j);
@@ -143,6 +145,7 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg) {
     p.dimg = oimg;
     p.row_lo = -j.above;
     p.row_hi = j.H + j.below;
+    p.pdl = pdl;
     p.g = j.gy;
     p.q = 2 * j.gy / B;
     p.r = 2 * j.gy % B;
@@ -258,7 +261,7 @@ cudaError_t run_compound(const MorphJob& j, void* tmp) {
     v.src = t2;
     v.sp = tp;
     v.simg = timg;
-    return run_v(v, j.dst, j.dp, j.dimg);
+    return run_v(v, j.dst, j.dp, j.dimg, 1);
 }
 
 size_t scratch_pitch(const MorphJob& j) { return ((size_t)j.W * j.elem + 255) & ~size_t(255); }
@@ -291,7 +294,7 @@ cudaError_t run(const MorphJob& j, void* tmp) {
         v.src = tmp;
         v.sp = tp;
         v.simg = timg;
-        return run_v(v, j.dst, j.dp, j.dimg);
+        return run_v(v, j.dst, j.dp, j.dimg, 1);
     }
     const int R = band_rows(j);
     const size_t timg = tp * (size_t)R;

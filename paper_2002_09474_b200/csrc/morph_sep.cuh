@@ -48,6 +48,7 @@ struct SepParams {
     int parts, pw;       // H: column parts per row group (one warp each), output columns per part
     int batch;
     int discard;         // H: discard the source lines after use (source = private scratch)
+    int pdl;             // launched as a programmatic dependent of the previous pass (same op)
     int nstrips, nbands; // V (TMA): 128-pixel strips per row, bands per image
     int nsl, nst;        // V (TMA): leading / trailing ring slots per warp
     int wsmem;           // V (TMA): shared-memory bytes per warp
@@ -283,7 +284,8 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
 #endif
 template <typename T, int MODE, int B, int QM>
 __global__ void __launch_bounds__(VT, SEP_VMINB) vpass_kernel(const SepParams p) {
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // H may start scheduling
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // a dependent may start scheduling
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // no-op unless launched as a PDL dependent
     const int c = blockIdx.x * VT + threadIdx.x;
     if (c >= p.nwords) return;
     const int y0 = blockIdx.y * p.rb;
@@ -318,7 +320,8 @@ __global__ void __launch_bounds__(VT) vtma_kernel(const SepParams p, const __gri
     constexpr int SB = 128 * sz;  // bytes per strip row
     constexpr int TB = B + VRMAX;  // rows per trailing box
     extern __shared__ __align__(128) unsigned char smem[];
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // H may start scheduling
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // a dependent may start scheduling
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // no-op unless launched as a PDL dependent
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wid = blockIdx.x * VTW + warp;
     const int per_img = p.nstrips * p.nbands;
@@ -727,11 +730,30 @@ __global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
     const int part = widx - gidx * p.parts;
     const int img = gidx / p.groups;
     const int grp = gidx - img * p.groups;
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // a dependent V may start scheduling
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // no-op unless launched as a PDL dependent
     if (img >= p.batch) return;  // whole warp: no shuffle partner is left behind
     const int y = grp * 4;
     h_item<T, MODE, C, BX, STAGES>(p, p.src + (size_t)img * p.simg + (size_t)y * p.sp, p.sp,
                            p.dst + (size_t)img * p.dimg + (size_t)y * p.dp, min(4, p.H - y), part);
+}
+
+// Launch with programmatic stream serialization when p.pdl: the CTAs may be scheduled while the
+// previous pass drains; the kernel's griddepcontrol.wait holds them until its results are visible.
+template <typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(SepParams, Args...), dim3 grid, dim3 block, int smem, cudaStream_t s,
+                              const SepParams& p, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = p.pdl && tune("sep_pdl", 0) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, p, args...);
 }
 
 // H launch: after a V pass into the scratch band (p.discard) H is a programmatic dependent launch
@@ -747,7 +769,7 @@ inline cudaError_t launch_hk(void (*kern)(SepParams), const SepParams& p, dim3 g
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = p.discard && tune("sep_pdl", 1) ? 1 : 0;
+    cfg.numAttrs = (p.discard || p.pdl) && tune("sep_pdl", 0) ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();

@@ -284,7 +284,8 @@ SEP_KNOBS = [
     {"sep_notma": 0, "sep_pf": 3, "sep_rb": 24},  # deeper TMA prefetch, short bands (more edge bands)
     {"sep_notma": 1, "sep_rb": 8},        # plain-load vertical pass, one block per band
     {"sep_l2mb": 0, "sep_parts": 3, "sep_hfirst": 0},  # vertical pass first, 64-row L2 bands, 3 parts
-    {"sep_parts": 1, "sep_pdl": 0, "sep_hfirst": 0},  # one warp per row group, no PDL, V first
+    {"sep_parts": 1, "sep_pdl": 1, "sep_hfirst": 0},  # one warp per row group, PDL between passes, V first
+    {"sep_pdl": 1},                       # PDL between the passes, H first
     {"sep_hh": 0},                        # opening / closing as four passes
 ]
 
