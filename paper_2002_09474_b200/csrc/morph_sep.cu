@@ -65,6 +65,14 @@ bool choose_c(int elem, int g, int* C_out) {
     return true;
 }
 
+// the TMA pipeline pays off on large images (16384^2 u8 1x63: 77% vs 65% of HBM); on small ones
+// the plain-load kernel ramps faster (4096^2: 13.0 vs 15.4 us) (tall images only: a band touching
+// the top or bottom border fills its rings synchronously)
+bool v_wants_tma(const MorphJob& j) {
+    const long long px = (long long)j.W * j.H * j.batch;
+    return env_int("sep_notma", px >= (1LL << 26) && j.H >= 2048 ? 0 : 1) == 0;
+}
+
 // TMA-fed variant when the maps encode (16-byte pitches); the plain LDG kernel otherwise.
 template <typename T, int MODE, int B>
 cudaError_t launch_v_t(const SepParams& p0, dim3 grid, cudaStream_t s, const MorphJob& j) {
@@ -74,9 +82,7 @@ cudaError_t launch_v_t(const SepParams& p0, dim3 grid, cudaStream_t s, const Mor
     // the TMA pipeline pays off on large images (16384^2 u8 1x63: 77% vs 65% of HBM); on small ones
     // the plain-load kernel ramps faster (4096^2: 13.0 vs 15.4 us)
     // (tall images only: a band touching the top or bottom border fills its rings synchronously)
-    const long long px = (long long)j.W * j.H * j.batch;
-    const int no_tma = env_int("sep_notma", px >= (1LL << 26) && j.H >= 2048 ? 0 : 1);
-    bool tma = !no_tma && stream::encode_input_map(j, SB / 4, B, &lmap) &&
+    const bool tma = !p.sstride && v_wants_tma(j) && stream::encode_input_map(j, SB / 4, B, &lmap) &&
                stream::encode_input_map(j, SB / 4, B + VRMAX, &tmap) && stream::encode_output_map(j, SB, B, &omap);
     if (tma) {
         const int pf = std::max(1, env_int("sep_pf", 1));
@@ -91,6 +97,9 @@ cudaError_t launch_v_t(const SepParams& p0, dim3 grid, cudaStream_t s, const Mor
         kernel_occupancy((const void*)kern, VT, smem, &e);
         if (e != cudaSuccess) return e;
         cudaError_t le = launch_pdl(kern, dim3((unsigned)((warps + VTW - 1) / VTW)), dim3(VT), smem, s, p, lmap, tmap, omap);
+        if (le != cudaSuccess) return le;
+    } else if (p.sstride) {  // strip-major intermediate: rows at compile-time offsets
+        cudaError_t le = launch_pdl(vpass_kernel<T, MODE, B, QM, SB>, grid, dim3(VT), 0, s, p);
         if (le != cudaSuccess) return le;
     } else {
         cudaError_t le = launch_pdl(vpass_kernel<T, MODE, B, QM>, grid, dim3(VT), 0, s, p);
@@ -133,7 +142,7 @@ SepParams base_params(const MorphJob& j) {
 }
 
 // One vertical pass over the job's rows: src (rows [-above, H + below) valid) -> out.
-cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl = 0) {
+cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl = 0, size_t sstride = 0) {
     int B = 0;
     if (!choose_b(j.elem, j.gy, &B)) return cudaErrorInvalidValue;
     SepParams p = base_params(j);
@@ -146,6 +155,7 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl 
     p.row_lo = -j.above;
     p.row_hi = j.H + j.below;
     p.pdl = pdl;
+    p.sstride = sstride;
     p.g = j.gy;
     p.q = 2 * j.gy / B;
     p.r = 2 * j.gy % B;
@@ -173,7 +183,8 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl 
 
 // One horizontal pass over H rows: in -> job dst (stages = 2: this mode then the other, the two
 // horizontal passes of an opening / closing).
-cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int discard, int stages = 1) {
+cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int discard, int stages = 1,
+                  size_t dsstride = 0) {
     int C = 0;
     if (!choose_c(j.elem, j.gx, &C)) return cudaErrorInvalidValue;
     SepParams p = base_params(j);
@@ -186,6 +197,7 @@ cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int
     p.g = j.gx;
     p.groups = (j.H + 3) / 4;
     p.discard = discard;
+    p.dsstride = dsstride;
     // parts: ~24 resident warps per SM, each part a whole number of segments
     const int A = stages * (j.gx / C + (j.gx % C ? 1 : 0));
     const int OS = (32 - 2 * A) * C;
@@ -278,23 +290,29 @@ cudaError_t run(const MorphJob& j, void* tmp) {
     if (j.gy == 0) return run_h(j, j.src, j.sp, j.simg, 0);
     if (j.gx == 0) return run_v(j, j.dst, j.dp, j.dimg);
     const size_t tp = scratch_pitch(j);
-    if (env_int("sep_hfirst", 1) && j.above == 0 && j.below == 0) {
+    if (env_int("sep_hfirst", 1) && j.above == 0 && j.below == 0 && band_rows(j) == j.H) {
         // Whole images: horizontal pass first (src -> scratch), vertical second (scratch -> dst).
         // The latency-bound vertical pass then reads its 2-3 copies of every row from L2 instead of
         // HBM (4096^2: 63x63 20.9 vs 23.5 us, 101x101 23.6 vs 26.0; 16384^2 equal); the scratch is
         // not discarded (several vertical bands read each row). Row bands (halo rows) keep V first.
-        const size_t timg = tp * (size_t)j.H;
+        // The vertical pass on loads (small / short images) reads a strip-major intermediate
+        // (128-pixel strips, rows 128*sz bytes apart): every row of a block is then an immediate
+        // offset from one base register.
+        const bool smaj = !v_wants_tma(j) && env_int("sep_strip", 1);
+        const size_t SB = (size_t)128 * j.elem;
+        const size_t sstride = SB * (size_t)j.H;
+        const size_t timg = smaj ? sstride * (size_t)((j.W + 127) / 128) : tp * (size_t)j.H;
         MorphJob h = j;
         h.dst = tmp;
-        h.dp = tp;
+        h.dp = smaj ? SB : tp;
         h.dimg = timg;
-        cudaError_t e = run_h(h, j.src, j.sp, j.simg, 0);
+        cudaError_t e = run_h(h, j.src, j.sp, j.simg, 0, 1, smaj ? sstride : 0);
         if (e != cudaSuccess) return e;
         MorphJob v = j;
         v.src = tmp;
-        v.sp = tp;
+        v.sp = smaj ? SB : tp;
         v.simg = timg;
-        return run_v(v, j.dst, j.dp, j.dimg, 1);
+        return run_v(v, j.dst, j.dp, j.dimg, 1, smaj ? sstride : 0);
     }
     const int R = band_rows(j);
     const size_t timg = tp * (size_t)R;

@@ -49,6 +49,8 @@ struct SepParams {
     int batch;
     int discard;         // H: discard the source lines after use (source = private scratch)
     int pdl;             // launched as a programmatic dependent of the previous pass (same op)
+    size_t sstride;      // V: source strip stride (strip-major intermediate) or 0 (row-major)
+    size_t dsstride;     // H: destination strip stride (strip-major intermediate) or 0 (row-major)
     int nstrips, nbands; // V (TMA): 128-pixel strips per row, bands per image
     int nsl, nst;        // V (TMA): leading / trailing ring slots per warp
     int wsmem;           // V (TMA): shared-memory bytes per warp
@@ -143,7 +145,9 @@ constexpr int VRMAX = 4;  // tail rows r = 2g mod B folded from re-read rows (pl
 //   G    = the r rows [base-2g+B, base-(q-1)B) u whole blocks L-q+1 .. L-1 (minima M[0..q-2]),
 //   P[m] = prefix of the leading block [base, base+m].
 // All 2B (+r) loads are issued before the first reduction (no branches between them).
-template <typename T, int MODE, int B, int QM, bool EDGE, bool FULL>
+// SPC: compile-time source row pitch (0 = runtime p.sp). With SPC every row of a block is a
+// compile-time offset from one base register (the strip-major intermediate of the H-first order).
+template <typename T, int MODE, int B, int QM, bool EDGE, bool FULL, int SPC>
 __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uint8_t* drow, int base, int nst,
                                        int nvalid, uint2 (&M)[QM]) {
     using V = VW<T>;
@@ -151,7 +155,7 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
     const int w1 = 2 * p.g, q = p.q, r = p.r;
     const uint2 ID = ident2<MODE>();
     const Raw CW = V::splat(p.bval);
-    const ptrdiff_t sp = (ptrdiff_t)p.sp;
+    const ptrdiff_t sp = SPC ? (ptrdiff_t)SPC : (ptrdiff_t)p.sp;
     auto ldE = [&](int i) -> Raw {  // border-aware (edge bands): clamp, then substitute the constant
         const int ic = min(max(i, p.row_lo), p.row_hi - 1);
         const Raw v = V::load(s + (ptrdiff_t)ic * sp);
@@ -164,6 +168,10 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
         if constexpr (EDGE) {
 #pragma unroll
             for (int m = 0; m < B; ++m) xl[m] = ldE(base + m);
+        } else if constexpr (SPC != 0) {
+            const uint8_t* pl = s + (ptrdiff_t)base * sp;
+#pragma unroll
+            for (int m = 0; m < B; ++m) xl[m] = V::load(pl + m * SPC);  // immediate offsets
         } else {
             const uint8_t* pl = s + (ptrdiff_t)base * sp;
 #pragma unroll
@@ -181,16 +189,25 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
             if (t < r) xr[t] = ldE(rb0 + t);
     } else {
         const uint8_t* pt = s + (ptrdiff_t)tb * sp;
+        if constexpr (SPC != 0) {
 #pragma unroll
-        for (int m = 0; m < B; ++m) {
-            xt[m] = V::load(pt);
-            pt += sp;
-        }
-        // the r tail rows follow the trailing batch directly (rb0 = tb + B)
+            for (int m = 0; m < B; ++m) xt[m] = V::load(pt + m * SPC);
+            // the r tail rows follow the trailing batch directly (rb0 = tb + B)
 #pragma unroll
-        for (int t = 0; t < VRMAX; ++t) {
-            if (t < r) xr[t] = V::load(pt);
-            pt += sp;
+            for (int t = 0; t < VRMAX; ++t)
+                if (t < r) xr[t] = V::load(pt + (B + t) * SPC);
+        } else {
+#pragma unroll
+            for (int m = 0; m < B; ++m) {
+                xt[m] = V::load(pt);
+                pt += sp;
+            }
+            // the r tail rows follow the trailing batch directly (rb0 = tb + B)
+#pragma unroll
+            for (int t = 0; t < VRMAX; ++t) {
+                if (t < r) xr[t] = V::load(pt);
+                pt += sp;
+            }
         }
     }
 #ifndef SEP_VSPLIT
@@ -232,10 +249,11 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
     M[0] = P;
 }
 
-template <typename T, int MODE, int B, int QM, bool EDGE>
+template <typename T, int MODE, int B, int QM, bool EDGE, int SPC = 0>
 __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s, uint8_t* d, int y0, int y1,
                                            int nvalid) {
     using V = VW<T>;
+    const ptrdiff_t sp = SPC ? (ptrdiff_t)SPC : (ptrdiff_t)p.sp;
     const int i0 = y0 + p.g;  // leading input row of output row y0
     const uint2 ID = ident2<MODE>();
     uint2 M[QM];
@@ -245,16 +263,18 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
     for (int L = -(p.q - 1); L < 0; ++L) {
         const int base = i0 + L * B;
         typename V::Raw x[B];
-        const uint8_t* pw = s + (ptrdiff_t)base * (ptrdiff_t)p.sp;
+        const uint8_t* pw = s + (ptrdiff_t)base * sp;
 #pragma unroll
         for (int m = 0; m < B; ++m) {
             if constexpr (EDGE) {
                 const int i = base + m;
                 const int ic = min(max(i, p.row_lo), p.row_hi - 1);
-                x[m] = V::sel(p.cmode && ic != i, V::splat(p.bval), V::load(s + (ptrdiff_t)ic * (ptrdiff_t)p.sp));
+                x[m] = V::sel(p.cmode && ic != i, V::splat(p.bval), V::load(s + (ptrdiff_t)ic * sp));
+            } else if constexpr (SPC != 0) {
+                x[m] = V::load(pw + m * SPC);
             } else {
                 x[m] = V::load(pw);
-                pw += p.sp;
+                pw += sp;
             }
         }
         uint2 P = V::unpack(x[0]);
@@ -268,8 +288,8 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
         const int base = i0 + (yb - y0);
         uint8_t* drow = d + (ptrdiff_t)yb * (ptrdiff_t)p.dp;
         const int nst = y1 - yb;
-        if (nst >= B && nvalid == 4) vblock<T, MODE, B, QM, EDGE, true>(p, s, drow, base, nst, nvalid, M);
-        else vblock<T, MODE, B, QM, EDGE, false>(p, s, drow, base, nst, nvalid, M);
+        if (nst >= B && nvalid == 4) vblock<T, MODE, B, QM, EDGE, true, SPC>(p, s, drow, base, nst, nvalid, M);
+        else vblock<T, MODE, B, QM, EDGE, false, SPC>(p, s, drow, base, nst, nvalid, M);
     }
 }
 
@@ -282,7 +302,7 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
 #ifndef SEP_VHOIST
 #define SEP_VSPLIT 1
 #endif
-template <typename T, int MODE, int B, int QM>
+template <typename T, int MODE, int B, int QM, int SPC = 0>
 __global__ void __launch_bounds__(VT, SEP_VMINB) vpass_kernel(const SepParams p) {
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // a dependent may start scheduling
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // no-op unless launched as a PDL dependent
@@ -292,13 +312,16 @@ __global__ void __launch_bounds__(VT, SEP_VMINB) vpass_kernel(const SepParams p)
     const int y1 = min(y0 + p.rb, p.H);
     const int nblk = (y1 - y0 + B - 1) / B;
     constexpr int sz = sizeof(T);
-    const uint8_t* s = p.src + (size_t)blockIdx.z * p.simg + (size_t)c * 4 * sz;
+    // source column word c: row-major (strip stride 0) or strip-major (128-pixel strips of
+    // p.sstride bytes, rows SPC bytes apart)
+    const uint8_t* s = p.src + (size_t)blockIdx.z * p.simg +
+                       (p.sstride ? (size_t)(c >> 5) * p.sstride + (size_t)(c & 31) * 4 * sz : (size_t)c * 4 * sz);
     uint8_t* d = p.dst + (size_t)blockIdx.z * p.dimg + (size_t)c * 4 * sz;
     // rows touched: [y0 - g, y0 + nblk*B - 1 + g]
     const bool edge = (y0 - p.g < p.row_lo) || (y0 + nblk * B + p.g > p.row_hi);
     const int nvalid = min(4, p.W - 4 * c);
-    if (edge) vpass_body<T, MODE, B, QM, true>(p, s, d, y0, y1, nvalid);
-    else vpass_body<T, MODE, B, QM, false>(p, s, d, y0, y1, nvalid);
+    if (edge) vpass_body<T, MODE, B, QM, true, SPC>(p, s, d, y0, y1, nvalid);
+    else vpass_body<T, MODE, B, QM, false, SPC>(p, s, d, y0, y1, nvalid);
 }
 
 // ---------------- V fed by TMA: one warp = one strip of 128 pixels x one band ------------------
@@ -688,7 +711,9 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
         uint32_t o0[NW], o1[NW], o2[NW], o3[NW];
         h_transpose_out<T, C>(o, o0, o1, o2, o3);
         if (lane >= HA && lane < 32 - HA && cx < W) {
-            uint8_t* drow = drow0 + (ptrdiff_t)cx * sz;
+            // a chunk never straddles a 128-pixel strip (C divides 128)
+            uint8_t* drow = drow0 + (p.dsstride ? (ptrdiff_t)(cx >> 7) * (ptrdiff_t)p.dsstride + (ptrdiff_t)(cx & 127) * sz
+                                                : (ptrdiff_t)cx * sz);
             if (cx + C <= W) {
                 h_store_row<T, C>(drow, o0);
                 if (nrows > 1) h_store_row<T, C>(drow + p.dp, o1);
