@@ -65,12 +65,13 @@ bool choose_c(int elem, int g, int* C_out) {
     return true;
 }
 
-// the TMA pipeline pays off on large images (16384^2 u8 1x63: 77% vs 65% of HBM); on small ones
-// the plain-load kernel ramps faster (4096^2: 13.0 vs 15.4 us) (tall images only: a band touching
-// the top or bottom border fills its rings synchronously)
+// The TMA pipeline pays off only on the largest images: with the strip-major intermediate the
+// plain-load vertical pass wins up to 16384^2 (8192^2 63x63: 70 vs 82 us; 16384^2 even) and the TMA
+// pass from 2^29 pixels (32768^2: 791 vs 816 us). Tall images only: a band touching the top or
+// bottom border fills its rings synchronously.
 bool v_wants_tma(const MorphJob& j) {
     const long long px = (long long)j.W * j.H * j.batch;
-    return env_int("sep_notma", px >= (1LL << 26) && j.H >= 2048 ? 0 : 1) == 0;
+    return env_int("sep_notma", px >= (1LL << 29) && j.H >= 2048 ? 0 : 1) == 0;
 }
 
 // TMA-fed variant when the maps encode (16-byte pitches); the plain LDG kernel otherwise.
@@ -169,7 +170,7 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl 
     // when the warm-up is 2x a band (4096^2 101x101: 25.5 vs 28.2 us at the old 2(q-1)B floor)
     // TMA path: bands of 320-640 rows (32768^2 63x63: rb 640 865 us, 160 895 us, one band per warp
     // per 2341 rows 1081 us)
-    if ((long long)j.W * j.H * j.batch >= (1LL << 26) && j.H >= 2048) rb = std::min(std::max(rb, 320), 640);
+    if (v_wants_tma(j)) rb = std::min(std::max(rb, 320), 640);
     rb = env_int("sep_rb", rb);
     rb = std::max(B, (rb + B - 1) / B * B);
     p.rb = rb;
