@@ -484,9 +484,12 @@ struct HChunk {
 template <typename T, int C>
 __device__ __forceinline__ void h_load_row(const uint8_t* p, uint32_t (&w)[HChunk<T, C>::NW]) {
     constexpr int NW = HChunk<T, C>::NW;
-    if constexpr (NW == 4) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
-        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    if constexpr (NW >= 4) {  // 16 or 32 bytes
+#pragma unroll
+        for (int k = 0; k < NW; k += 4) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + k / 4);
+            w[k] = v.x; w[k + 1] = v.y; w[k + 2] = v.z; w[k + 3] = v.w;
+        }
     } else {
         const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
         w[0] = v.x; w[1] = v.y;
@@ -495,8 +498,12 @@ __device__ __forceinline__ void h_load_row(const uint8_t* p, uint32_t (&w)[HChun
 template <typename T, int C>
 __device__ __forceinline__ void h_store_row(uint8_t* p, const uint32_t (&w)[HChunk<T, C>::NW]) {
     constexpr int NW = HChunk<T, C>::NW;
-    if constexpr (NW == 4) *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
-    else *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+    if constexpr (NW >= 4) {
+#pragma unroll
+        for (int k = 0; k < NW; k += 4) reinterpret_cast<uint4*>(p)[k / 4] = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+    } else {
+        *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+    }
 }
 
 // Border-aware load of one lane chunk row (chunks that reach past column 0 or W-1). Chunks start
@@ -721,10 +728,16 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
                 if (nrows > 3) h_store_row<T, C>(drow + 3 * p.dp, o3);
             } else {
                 const int n = W - cx;
-                auto part_store = [&](int k, const uint32_t (&rw)[NW]) {
-                    if (k < nrows)
-                        for (int e = 0; e < n; ++e)
-                            reinterpret_cast<T*>(drow + (size_t)k * p.dp)[e] = (T)(rw[(e * sz) / 4] >> ((e * sz * 8) & 31));
+                auto part_store = [&](int k, const uint32_t (&rw)[NW]) {  // compile-time indices only
+                    if (k < nrows) {
+#pragma unroll
+                        for (int wi = 0; wi < NW; ++wi)
+#pragma unroll
+                            for (int b = 0; b < 4 / sz; ++b) {
+                                const int e = wi * (4 / sz) + b;
+                                if (e < n) reinterpret_cast<T*>(drow + (size_t)k * p.dp)[e] = (T)(rw[wi] >> (8 * sz * b));
+                            }
+                    }
                 };
                 part_store(0, o0);
                 part_store(1, o1);
