@@ -15,6 +15,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "../../include/rmgpu.h"
 #include "common.cuh"
@@ -428,10 +429,12 @@ int run_morph(const void* src, size_t sp, size_t simg, void* dst, size_t dp, siz
     return rc;
 }
 
-// Internal per-thread stream + cached pool for the synchronous host entry points.
+// Internal per-thread streams + cached pool for the synchronous host entry points: `stream` runs
+// the kernels, `up` / `down` carry the host->device and device->host copies of a pipelined call.
 struct HostCtx {
     int device = -1;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr, up = nullptr, down = nullptr;
+    std::vector<cudaEvent_t> events;
 };
 thread_local HostCtx t_ctx;
 
@@ -442,9 +445,21 @@ int host_stream(cudaStream_t* out) {
     RM_CUDA(cudaGetDevice(&dev));
     if (t_ctx.stream == nullptr || t_ctx.device != dev) {
         RM_CUDA(cudaStreamCreateWithFlags(&t_ctx.stream, cudaStreamNonBlocking));
+        RM_CUDA(cudaStreamCreateWithFlags(&t_ctx.up, cudaStreamNonBlocking));
+        RM_CUDA(cudaStreamCreateWithFlags(&t_ctx.down, cudaStreamNonBlocking));
+        t_ctx.events.clear();
         t_ctx.device = dev;
     }
     *out = t_ctx.stream;
+    return RMGPU_OK;
+}
+
+int host_events(size_t n) {
+    while (t_ctx.events.size() < n) {
+        cudaEvent_t e;
+        RM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        t_ctx.events.push_back(e);
+    }
     return RMGPU_OK;
 }
 
@@ -468,11 +483,56 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     a.s = b.s = s;
     RM_CUDA(scratch_alloc(&a.p, pitch * H, s));
     RM_CUDA(scratch_alloc(&b.p, pitch * H, s));
-    RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, rb, H, cudaMemcpyHostToDevice, s));
-    rc = run_morph(a.p, pitch, 0, b.p, pitch, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, elem, s);
-    if (rc) return rc;
-    RM_CUDA(cudaMemcpy2DAsync(hdst, dp, b.p, pitch, rb, H, cudaMemcpyDeviceToHost, s));
+    // Pipelined over row bands: band k uploads on `up`, is computed on `stream` once the band below
+    // it has arrived too (its halo rows; bands are at least one halo tall), and downloads on `down`
+    // while later bands still upload -- the two copy directions overlap each other and the kernels.
+    const int halo = (op == RMGPU_OPEN || op == RMGPU_CLOSE) ? 2 * (wy / 2) : wy / 2;
+    const int nb_target = rmgpu::tune("host_bands", 4);  // 4096^2: 0.65 -> 0.56 ms per call (PCIe-bound)
+    const int R = std::max({halo, 64, (H + nb_target - 1) / std::max(1, nb_target)});
+    const int nb = (H + R - 1) / R;
+    if (nb < 2) {
+        RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, rb, H, cudaMemcpyHostToDevice, s));
+        rc = run_morph(a.p, pitch, 0, b.p, pitch, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, elem, s);
+        if (rc) return rc;
+        RM_CUDA(cudaMemcpy2DAsync(hdst, dp, b.p, pitch, rb, H, cudaMemcpyDeviceToHost, s));
+        RM_CUDA(cudaStreamSynchronize(s));
+        return RMGPU_OK;
+    }
+    if ((rc = host_events(2 * (size_t)nb + 1))) return rc;
+    cudaEvent_t* ev_in = t_ctx.events.data();
+    cudaEvent_t* ev_out = ev_in + nb;
+    cudaEvent_t ev_start = ev_in[2 * nb];
+    // the scratch allocations are stream-ordered on `s`: the copy streams start after them
+    RM_CUDA(cudaEventRecord(ev_start, s));
+    RM_CUDA(cudaStreamWaitEvent(t_ctx.up, ev_start, 0));
+    // contiguous host rows (pitch == row bytes == device pitch) go as plain 1-D copies
+    const bool flat_in = sp == rb && pitch == rb, flat_out = dp == rb && pitch == rb;
+    for (int k = 0; k < nb; ++k) {
+        const int r0 = k * R, n = std::min(R, H - r0);
+        char* d = static_cast<char*>(a.p) + (size_t)r0 * pitch;
+        const char* h = static_cast<const char*>(hsrc) + (size_t)r0 * sp;
+        if (flat_in) RM_CUDA(cudaMemcpyAsync(d, h, rb * n, cudaMemcpyHostToDevice, t_ctx.up));
+        else RM_CUDA(cudaMemcpy2DAsync(d, pitch, h, sp, rb, n, cudaMemcpyHostToDevice, t_ctx.up));
+        RM_CUDA(cudaEventRecord(ev_in[k], t_ctx.up));
+    }
+    for (int k = 0; k < nb; ++k) {
+        const int r0 = k * R, n = std::min(R, H - r0);
+        RM_CUDA(cudaStreamWaitEvent(s, ev_in[std::min(k + 1, nb - 1)], 0));  // band k and its halo
+        const int above = std::min(halo, r0), below = std::min(halo, H - r0 - n);
+        rc = run_morph(static_cast<char*>(a.p) + (size_t)r0 * pitch, pitch, 0,
+                       static_cast<char*>(b.p) + (size_t)r0 * pitch, pitch, 0, 1, W, n, above, below, wx, wy, op,
+                       border, bval, elem, s);
+        if (rc) return rc;
+        RM_CUDA(cudaEventRecord(ev_out[k], s));
+        RM_CUDA(cudaStreamWaitEvent(t_ctx.down, ev_out[k], 0));
+        char* h = static_cast<char*>(hdst) + (size_t)r0 * dp;
+        const char* d = static_cast<const char*>(b.p) + (size_t)r0 * pitch;
+        if (flat_out) RM_CUDA(cudaMemcpyAsync(h, d, rb * n, cudaMemcpyDeviceToHost, t_ctx.down));
+        else RM_CUDA(cudaMemcpy2DAsync(h, dp, d, pitch, rb, n, cudaMemcpyDeviceToHost, t_ctx.down));
+    }
+    RM_CUDA(cudaStreamSynchronize(t_ctx.down));
     RM_CUDA(cudaStreamSynchronize(s));
+    // the buffers are freed on `s` (DevBuf): every copy that used them has completed
     return RMGPU_OK;
 }
 
