@@ -684,29 +684,29 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
     // rows past the last one re-read it; their results are never stored
     const size_t rs1 = nrows > 1 ? sp : 0, rs2 = nrows > 2 ? 2 * sp : rs1, rs3 = nrows > 3 ? 3 * sp : rs2;
 
-    uint32_t r0[NW], r1[NW], r2[NW], r3[NW];
-    auto load_seg = [&](int X) {
+    using RowW = uint32_t[NW];
+    auto load_seg = [&](int X, RowW& q0, RowW& q1, RowW& q2, RowW& q3) {
         const int cx = X + (lane - HA) * C;
         if (cx >= 0 && cx + C <= W) {
             const uint8_t* b = srow0 + (ptrdiff_t)cx * sz;
-            h_load_row<T, C>(b, r0);
-            h_load_row<T, C>(b + rs1, r1);
-            h_load_row<T, C>(b + rs2, r2);
-            h_load_row<T, C>(b + rs3, r3);
+            h_load_row<T, C>(b, q0);
+            h_load_row<T, C>(b + rs1, q1);
+            h_load_row<T, C>(b + rs2, q2);
+            h_load_row<T, C>(b + rs3, q3);
         } else {
-            h_load_row_edge<T, C>(srow0, cx, W, p.cmode, p.bval, r0);
-            h_load_row_edge<T, C>(srow0 + rs1, cx, W, p.cmode, p.bval, r1);
-            h_load_row_edge<T, C>(srow0 + rs2, cx, W, p.cmode, p.bval, r2);
-            h_load_row_edge<T, C>(srow0 + rs3, cx, W, p.cmode, p.bval, r3);
+            h_load_row_edge<T, C>(srow0, cx, W, p.cmode, p.bval, q0);
+            h_load_row_edge<T, C>(srow0 + rs1, cx, W, p.cmode, p.bval, q1);
+            h_load_row_edge<T, C>(srow0 + rs2, cx, W, p.cmode, p.bval, q2);
+            h_load_row_edge<T, C>(srow0 + rs3, cx, W, p.cmode, p.bval, q3);
         }
     };
     const int xlo = part * p.pw, xhi = min(W, xlo + p.pw);
-    load_seg(xlo);
-    for (int X = xlo; X < xhi; X += OS) {
+    // reduce the segment at X held in q*, refilling q* with the segment at Xn (if any) first
+    auto process = [&](int X, RowW& q0, RowW& q1, RowW& q2, RowW& q3, int Xn) {
         const int cx = X + (lane - HA) * C;  // first column of this lane's chunk
         uint2 x[C];
-        h_transpose_in<T, C>(r0, r1, r2, r3, x);
-        if (X + OS < xhi) load_seg(X + OS);
+        h_transpose_in<T, C>(q0, q1, q2, q3, x);
+        if (Xn < xhi) load_seg(Xn, q0, q1, q2, q3);
         uint2 o[C];
         h_lane_pass<MODE, C, BX>(x, a, o);
         if constexpr (STAGES == 2) {
@@ -745,7 +745,12 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
                 part_store(3, o3);
             }
         }
-    }
+    };
+    // one segment in flight (measured: a second register set for two is slower -- 4096^2 63x1
+    // 10.3 -> 14.4 us -- code size and registers)
+    uint32_t r0[NW], r1[NW], r2[NW], r3[NW];
+    load_seg(xlo, r0, r1, r2, r3);
+    for (int X = xlo; X < xhi; X += OS) process(X, r0, r1, r2, r3, X + OS);
     if (p.discard) {
         // drop the source lines only this warp reads (its part minus the halos the neighbouring
         // parts read) from L2 unwritten: the source is a private scratch band
