@@ -291,6 +291,30 @@ SEP_KNOBS = [
 ]
 
 
+@pytest.mark.parametrize("knobs", [{}, {"sep_notma": 0}, {"sep_hfirst": 0, "sep_notma": 0}])
+def test_sep_large_shapes(gpu, restatement, knobs):
+    # K3 on images wide and tall enough for many strips, column parts and row bands (both pass
+    # orders; the TMA vertical pass forced on), ragged widths, every op, both borders
+    rng = np.random.default_rng(4242 + len(knobs))
+    for k, v in knobs.items():
+        gpu.debug_set(k, v)
+    try:
+        for c in range(6):
+            dtype = np.uint8 if c % 3 else np.uint16
+            es = np.dtype(dtype).itemsize
+            w, h = int(rng.integers(1500, 4200)), int(rng.integers(300, 1300))
+            g = int(rng.integers(4, 60))
+            wx, wy = 2 * g + 1, 2 * int(rng.integers(4, 60)) + 1
+            op, border = c % 5, int(rng.integers(0, 2))
+            bval = int(rng.integers(0, int(np.iinfo(dtype).max) + 1))
+            img = restatement.generate(w, h, 7000 + c, dtype=dtype)
+            got, _ = gpu_morph(gpu, img, wx, wy, op, border, bval, (-w) % (16 // es))
+            assert np.array_equal(got, restatement.morph(img, wx, wy, op, border, bval)), (knobs, c, w, h, wx, wy, op)
+    finally:
+        for k in knobs:
+            gpu.debug_set(k, -1)
+
+
 @pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
 def test_phase_kernel_fuzz(gpu, restatement, dtype):
     # K2 (persistent phase kernel) with K3 switched off: it stays the path for windows K3 declines
