@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "morph_sep.cuh"
 
@@ -75,6 +76,13 @@ bool v_wants_tma(const MorphJob& j) {
     const long long px = (long long)j.W * j.H * j.batch;
     return env_int("sep_notma", px >= (1LL << 29) && j.H >= 2048 ? 0 : 1) == 0;
 }
+// Strip-major source: a strip's block is one contiguous run -> 1-D bulk copies into the same TMA
+// pipeline (no tensor maps); pays off from 2^28 pixels (16384^2 63x63: 215 vs 228 us), the plain
+// loads ramp faster below (4096^2: 18.5 vs 23.5 us).
+bool v_wants_bulk(const MorphJob& j) {
+    const long long px = (long long)j.W * j.H * j.batch;
+    return env_int("sep_vbulk", px >= (1LL << 28) && j.H >= 2048 ? 1 : 0) != 0;
+}
 
 // TMA-fed variant when the maps encode (16-byte pitches); the plain LDG kernel otherwise.
 template <typename T, int MODE, int B>
@@ -85,8 +93,15 @@ cudaError_t launch_v_t(const SepParams& p0, dim3 grid, cudaStream_t s, const Mor
     // the TMA pipeline pays off on large images (16384^2 u8 1x63: 77% vs 65% of HBM); on small ones
     // the plain-load kernel ramps faster (4096^2: 13.0 vs 15.4 us)
     // (tall images only: a band touching the top or bottom border fills its rings synchronously)
-    const bool tma = !p.sstride && v_wants_tma(j) && stream::encode_input_map(j, SB / 4, B, &lmap) &&
-               stream::encode_input_map(j, SB / 4, B + VRMAX, &tmap) && stream::encode_output_map(j, SB, B, &omap);
+    // strip-major source: the bulk-copy variant (no input maps) when sep_vbulk; else plain loads
+    const bool bulk = p.sstride && v_wants_bulk(j) && stream::encode_output_map(j, SB, B, &omap);
+    if (bulk) {
+        memset(&lmap, 0, sizeof lmap);
+        memset(&tmap, 0, sizeof tmap);
+    }
+    const bool tma = bulk || (!p.sstride && v_wants_tma(j) && stream::encode_input_map(j, SB / 4, B, &lmap) &&
+                              stream::encode_input_map(j, SB / 4, B + VRMAX, &tmap) &&
+                              stream::encode_output_map(j, SB, B, &omap));
     if (tma) {
         const int pf = std::max(1, env_int("sep_pf", 1));
         p.nsl = p.nst = pf + 1;
@@ -172,7 +187,7 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl 
     // when the warm-up is 2x a band (4096^2 101x101: 25.5 vs 28.2 us at the old 2(q-1)B floor)
     // TMA path: bands of 320-640 rows (32768^2 63x63: rb 640 865 us, 160 895 us, one band per warp
     // per 2341 rows 1081 us)
-    if (v_wants_tma(j)) rb = std::min(std::max(rb, 320), 640);
+    if (sstride ? v_wants_bulk(j) : v_wants_tma(j)) rb = std::min(std::max(rb, 320), sstride ? 320 : 640);
     rb = env_int("sep_rb", rb);
     rb = std::max(B, (rb + B - 1) / B * B);
     p.rb = rb;
@@ -301,7 +316,9 @@ cudaError_t run(const MorphJob& j, void* tmp) {
         // The vertical pass on loads (small / short images) reads a strip-major intermediate
         // (128-pixel strips, rows 128*sz bytes apart): every row of a block is then an immediate
         // offset from one base register.
-        const bool smaj = !v_wants_tma(j) && env_int("sep_strip", 1);
+        // (from 2^29 pixels the row-major intermediate + tensor-map TMA pass measured faster:
+        // 32768^2 63x63 796 vs 809 us)
+        const bool smaj = !v_wants_tma(j) && env_int("sep_strip", 1) != 0;
         const size_t SB = (size_t)128 * j.elem;
         const size_t sstride = SB * (size_t)j.H;
         const size_t timg = smaj ? sstride * (size_t)((j.W + 127) / 128) : tp * (size_t)j.H;

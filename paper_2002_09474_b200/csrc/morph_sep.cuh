@@ -360,7 +360,9 @@ __global__ void __launch_bounds__(VT) vtma_kernel(const SepParams p, const __gri
     // bands whose rows reach past the valid input rows fill the rings themselves (clamped rows /
     // the constant), synchronously; everything downstream is shared with the TMA path
     const bool edge = (y0 - g < p.row_lo) || (y0 + nblk * B + g > p.row_hi);
-    const uint8_t* ecol = p.src + (size_t)img * p.simg + (size_t)min(strip * 32 + lane, p.nwords - 1) * 4 * sz;
+    const int ecw = min(strip * 32 + lane, p.nwords - 1);
+    const uint8_t* ecol = p.src + (size_t)img * p.simg +
+                          (p.sstride ? (size_t)(ecw >> 5) * p.sstride + (size_t)(ecw & 31) * 4 * sz : (size_t)ecw * 4 * sz);
     auto fill = [&](unsigned char* slot, int row0, int nrows) {
         const Raw CW = V::splat(p.bval);
         for (int m = 0; m < nrows; ++m) {
@@ -387,16 +389,23 @@ __global__ void __launch_bounds__(VT) vtma_kernel(const SepParams p, const __gri
     const int i0 = y0 + g;  // leading input row of output row y0
     const int nL = q - 1 + nblk;
     const int xw = strip * (SB / 4);  // map x coordinate (32-bit words)
+    // strip-major source (p.sstride): a block of a strip is one contiguous run of rows -> one 1-D
+    // bulk copy, no tensor map
+    const uint8_t* sstrip = p.src + (size_t)img * p.simg + (size_t)strip * p.sstride;
     auto issue_lead = [&](int jl, int slot) {
         mbar_arrive_tx(&fl[slot], (uint32_t)(B * SB));
-        tma_box(lring + (size_t)slot * B * SB, &lmap, xw, i0 + (jl - (q - 1)) * B - p.row_lo, img, &fl[slot]);
+        const int row = i0 + (jl - (q - 1)) * B;
+        if (p.sstride) bulk_g2s(lring + (size_t)slot * B * SB, sstrip + (ptrdiff_t)row * SB, (uint32_t)(B * SB), &fl[slot]);
+        else tma_box(lring + (size_t)slot * B * SB, &lmap, xw, row - p.row_lo, img, &fl[slot]);
     };
     auto issue_trail = [&](int L, int slot) {
         mbar_arrive_tx(&ft[slot], (uint32_t)(TB * SB));
-        tma_box(tring + (size_t)slot * TB * SB, &tmap, xw, i0 + L * B - w1 - p.row_lo, img, &ft[slot]);
+        const int row = i0 + L * B - w1;
+        if (p.sstride) bulk_g2s(tring + (size_t)slot * TB * SB, sstrip + (ptrdiff_t)row * SB, (uint32_t)(TB * SB), &ft[slot]);
+        else tma_box(tring + (size_t)slot * TB * SB, &tmap, xw, row - p.row_lo, img, &ft[slot]);
     };
     if (lane == 0 && !edge) {
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&lmap) : "memory");
+        if (!p.sstride) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&lmap) : "memory");
         for (int k = 0; k < NSL && k < nL; ++k) issue_lead(k, k);
         for (int k = 0; k < NST && k < nblk; ++k) issue_trail(k, k);
     }

@@ -288,10 +288,11 @@ SEP_KNOBS = [
     {"sep_pdl": 1},                       # PDL between the passes, H first
     {"sep_hh": 0},                        # opening / closing as four passes
     {"sep_strip": 0},                     # H first into a row-major intermediate (not strip-major)
+    {"sep_vbulk": 1, "sep_pf": 2},        # strip-major intermediate read by 1-D bulk copies (TMA pipeline)
 ]
 
 
-@pytest.mark.parametrize("knobs", [{}, {"sep_notma": 0}, {"sep_hfirst": 0, "sep_notma": 0}])
+@pytest.mark.parametrize("knobs", [{}, {"sep_notma": 0}, {"sep_hfirst": 0, "sep_notma": 0}, {"sep_vbulk": 1}])
 def test_sep_large_shapes(gpu, restatement, knobs):
     # K3 on images wide and tall enough for many strips, column parts and row bands (both pass
     # orders; the TMA vertical pass forced on), ragged widths, every op, both borders
