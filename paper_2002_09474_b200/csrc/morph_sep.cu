@@ -304,33 +304,41 @@ int band_rows(const MorphJob& j) {
     return (int)std::min<long long>(rows, j.H);
 }
 
+// H-first order (with its whole intermediate in one scratch) unless the image is too large for it
+bool hfirst(const MorphJob& j) { return env_int("sep_hfirst", 1) && band_rows(j) == j.H; }
+
 cudaError_t run(const MorphJob& j, void* tmp) {
     if (j.gy == 0) return run_h(j, j.src, j.sp, j.simg, 0);
     if (j.gx == 0) return run_v(j, j.dst, j.dp, j.dimg);
     const size_t tp = scratch_pitch(j);
-    if (env_int("sep_hfirst", 1) && j.above == 0 && j.below == 0 && band_rows(j) == j.H) {
-        // Whole images: horizontal pass first (src -> scratch), vertical second (scratch -> dst).
-        // The latency-bound vertical pass then reads its 2-3 copies of every row from L2 instead of
-        // HBM (4096^2: 63x63 20.9 vs 23.5 us, 101x101 23.6 vs 26.0; 16384^2 equal); the scratch is
-        // not discarded (several vertical bands read each row). Row bands (halo rows) keep V first.
+    if (hfirst(j)) {
+        // Horizontal pass first (src -> scratch, halo rows of a row band included), vertical second
+        // (scratch -> dst). The latency-bound vertical pass then reads its 2-3 copies of every row
+        // from L2 instead of HBM (4096^2: 63x63 20.9 vs 23.5 us, 101x101 23.6 vs 26.0); the scratch
+        // is not discarded (several vertical bands read each row).
         // The vertical pass on loads (small / short images) reads a strip-major intermediate
         // (128-pixel strips, rows 128*sz bytes apart): every row of a block is then an immediate
         // offset from one base register.
         // (from 2^29 pixels the row-major intermediate + tensor-map TMA pass measured faster:
         // 32768^2 63x63 796 vs 809 us)
+        const int IH = j.H + j.above + j.below;
         const bool smaj = !v_wants_tma(j) && env_int("sep_strip", 1) != 0;
         const size_t SB = (size_t)128 * j.elem;
-        const size_t sstride = SB * (size_t)j.H;
-        const size_t timg = smaj ? sstride * (size_t)((j.W + 127) / 128) : tp * (size_t)j.H;
+        const size_t sstride = SB * (size_t)IH;
+        const size_t rowp = smaj ? SB : tp;
+        const size_t timg = smaj ? sstride * (size_t)((j.W + 127) / 128) : tp * (size_t)IH;
         MorphJob h = j;
+        h.src = static_cast<const uint8_t*>(j.src) - (ptrdiff_t)j.above * (ptrdiff_t)j.sp;
+        h.H = IH;
+        h.above = h.below = 0;
         h.dst = tmp;
-        h.dp = smaj ? SB : tp;
+        h.dp = rowp;
         h.dimg = timg;
-        cudaError_t e = run_h(h, j.src, j.sp, j.simg, 0, 1, smaj ? sstride : 0);
+        cudaError_t e = run_h(h, h.src, j.sp, j.simg, 0, 1, smaj ? sstride : 0);
         if (e != cudaSuccess) return e;
-        MorphJob v = j;
-        v.src = tmp;
-        v.sp = smaj ? SB : tp;
+        MorphJob v = j;  // rows [-above, H + below) of the scratch are valid
+        v.src = static_cast<uint8_t*>(tmp) + (size_t)j.above * rowp;
+        v.sp = rowp;
         v.simg = timg;
         return run_v(v, j.dst, j.dp, j.dimg, 1, smaj ? sstride : 0);
     }
@@ -356,6 +364,7 @@ cudaError_t run(const MorphJob& j, void* tmp) {
 
 size_t scratch_bytes(const MorphJob& j) {
     if (j.gx == 0 || j.gy == 0) return 0;
+    if (hfirst(j)) return scratch_pitch(j) * (size_t)(j.H + j.above + j.below) * (size_t)j.batch;
     return scratch_pitch(j) * (size_t)band_rows(j) * (size_t)j.batch;
 }
 
