@@ -2,27 +2,31 @@
 //
 // The reference computes a w_x x w_y erosion/dilation as a vertical pass into a full intermediate
 // image followed by a horizontal pass (separable.cpp:130-157; van Herk / Gil-Werman for long
-// windows, sliding_extrema.cpp:58-132). On B200 the intermediate of a 4096^2 u8 image (16 MB) fits
-// the 126 MB L2 many times over, so K3 keeps the reference's two-pass structure and makes each pass
-// a barrier-free, shared-memory-free streaming kernel:
+// windows, sliding_extrema.cpp:58-132). The passes commute (the border clamp is per axis), and on
+// B200 the intermediate of a 4096^2 u8 image (16 MB) fits the 126 MB L2 many times over, so K3
+// runs the two passes as barrier-free, shared-memory-free streaming kernels (planner and pass
+// order in morph_sep.cu: horizontal first on whole images and row bands):
 //
 //  * V (vertical pass): one thread per 4-pixel column word streams down a band of rows with
 //    plain coalesced loads. Block van Herk with blocks of B rows: out = min3(T[m], G, P[m]) where
 //    P is the running prefix of the leading block, T the suffix of the trailing rows (re-read: they
-//    were loaded w_y rows earlier and are still in L2) and G the minimum of the q-1 whole blocks in
-//    between (block minima kept in registers). Nothing is staged in shared memory.
-//  * H (horizontal pass): one warp per group of 4 rows sweeps the row in segments of 32 lane
+//    were loaded w_y rows earlier and are still in L2) and G the r tail rows plus the minimum of
+//    the q-1 whole blocks in between (block minima kept in registers). Reading the strip-major
+//    intermediate (128-pixel strips) the row pitch is a compile-time constant, so every row of a
+//    block is an immediate offset from one register. Large images: the same algorithm fed by a
+//    per-warp TMA pipeline (tensor boxes or 1-D bulk copies, output by TMA store).
+//  * H (horizontal pass): one warp per (group of 4 rows, column part) sweeps segments of 32 lane
 //    chunks of C columns. Each lane transposes its 4 x C pixels in registers (PRMT) so that the two
 //    16-bit lanes of a word hold different ROWS of one column, scans prefix and suffix along its C
 //    columns, and fetches the far suffix / prefix / chunk minima from the lanes a = g / C away with
-//    SHFL (g mod C is a template parameter, so every register index is compile-time).
+//    SHFL (g mod C is a template parameter, so every register index is compile-time). STAGES = 2
+//    runs an opening's / closing's two horizontal passes in one sweep.
 //  * Pixels use 16-bit SIMD lanes (VIMNMX(3).U16x2). u8 words keep their raw bytes: the 16-bit
 //    min/max of raw words is exact in the high byte of each lane, so a word A = raw carries pixels
 //    1 and 3 and A << 8 carries pixels 0 and 2 (no unpacking; one PRMT repacks).
 //
-// The intermediate is a private scratch buffer: the H pass discards every line it has finished
-// with (discard.global.L2), so it is never written back to HBM. HBM traffic = 1 read of the input
-// + 1 write of the output, the algorithmic minimum.
+// The intermediate is a private scratch buffer that is consumed while it is still in L2 (measured
+// DRAM traffic of a 4096^2 op: 33.9 MB for 33.5 MB algorithmic; profiles/traffic_cfg2.json).
 #pragma once
 
 #include "morph_stream.cuh"  // TMA / mbarrier helpers, tensor-map encoders
