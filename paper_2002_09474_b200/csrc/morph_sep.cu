@@ -183,8 +183,9 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl 
     const int sms = device_sm_count();
     int bands = (int)std::max(1LL, ((long long)sms * 24 * 32 + cols - 1) / cols);
     int rb = (j.H + bands - 1) / bands;
-    // no floor for the warm-up (q-1 blocks per band): cfg2 measured best with ~24 warps/SM even
-    // when the warm-up is 2x a band (4096^2 101x101: 25.5 vs 28.2 us at the old 2(q-1)B floor)
+    // the band is at least as tall as its warm-up (q-1 blocks): 4096^2 101x101 20.5 vs 21.6 us at
+    // 40 rows, 63x63 flat; a 2(q-1)B floor was slower (fewer warps)
+    rb = std::max(rb, (p.q - 1) * B);
     // TMA path: bands of 320-640 rows (32768^2 63x63: rb 640 865 us, 160 895 us, one band per warp
     // per 2341 rows 1081 us)
     if (sstride ? v_wants_bulk(j) : v_wants_tma(j)) rb = std::min(std::max(rb, 320), sstride ? 320 : 640);
