@@ -478,7 +478,9 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     if (W == 0 || H == 0) return RMGPU_OK;
     cudaStream_t s;
     if ((rc = host_stream(&s))) return rc;
-    const size_t rb = (size_t)W * elem, pitch = (rb + 255) & ~size_t(255);
+    // device rows as tight as the kernels allow (16-byte pitch): a host image whose rows are
+    // already that tight then moves as one flat copy instead of a 2-D copy of H short rows
+    const size_t rb = (size_t)W * elem, pitch = rb % 16 == 0 ? rb : (rb + 255) & ~size_t(255);
     DevBuf a, b;
     a.s = b.s = s;
     RM_CUDA(scratch_alloc(&a.p, pitch * H, s));
@@ -493,10 +495,12 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     const int R = std::max({halo, 64, (H + nb_target - 1) / std::max(1, nb_target)});
     const int nb = (H + R - 1) / R;
     if (nb < 2) {
-        RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, rb, H, cudaMemcpyHostToDevice, s));
+        if (sp == rb && pitch == rb) RM_CUDA(cudaMemcpyAsync(a.p, hsrc, rb * H, cudaMemcpyHostToDevice, s));
+        else RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, rb, H, cudaMemcpyHostToDevice, s));
         rc = run_morph(a.p, pitch, 0, b.p, pitch, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, elem, s);
         if (rc) return rc;
-        RM_CUDA(cudaMemcpy2DAsync(hdst, dp, b.p, pitch, rb, H, cudaMemcpyDeviceToHost, s));
+        if (dp == rb && pitch == rb) RM_CUDA(cudaMemcpyAsync(hdst, b.p, rb * H, cudaMemcpyDeviceToHost, s));
+        else RM_CUDA(cudaMemcpy2DAsync(hdst, dp, b.p, pitch, rb, H, cudaMemcpyDeviceToHost, s));
         RM_CUDA(cudaStreamSynchronize(s));
         return RMGPU_OK;
     }
