@@ -287,6 +287,7 @@ SEP_KNOBS = [
     {"sep_parts": 1, "sep_pdl": 1, "sep_hfirst": 0},  # one warp per row group, PDL between passes, V first
     {"sep_pdl": 1},                       # PDL between the passes, H first
     {"sep_hh": 0},                        # opening / closing as four passes
+    {"sep_hh": 2},                        # opening / closing always in three (also 16-column chunks)
     {"sep_strip": 0},                     # H first into a row-major intermediate (not strip-major)
     {"sep_vbulk": 1, "sep_pf": 2},        # strip-major intermediate read by 1-D bulk copies (TMA pipeline)
 ]
