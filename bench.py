@@ -694,8 +694,8 @@ def main(argv=None):
         e2e_px = getattr(wl, "e2e_pixels_per_step", wl.out_pixels_per_step)()
         e2e = {"value": dist.world * e2e_px * args.steps / e2e_s / 1e9, "unit": "Gpixel/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": getattr(wl, "e2e_path", "C-ABI rmgpu_morph_host_u8 per op (pinned host buffers, H2D + kernel + "
-                                                 "D2H, synchronous)")}
+               "path": getattr(wl, "e2e_path", "C-ABI rmgpu_morph_host_u8 per op (pinned host buffers; the call "
+                                                 "pipelines H2D, kernels and D2H over row bands; synchronous)")}
 
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:

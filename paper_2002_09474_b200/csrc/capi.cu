@@ -491,7 +491,7 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     const int halo = (op == RMGPU_OPEN || op == RMGPU_CLOSE) ? 2 * (wy / 2) : wy / 2;
     // 4096^2: 0.65 -> 0.56 ms per call (PCIe-bound); small images (1920x1080) lose more to the
     // per-band API calls than they gain from the overlap
-    const int nb_target = rmgpu::tune("host_bands", rb * (size_t)H >= ((size_t)8 << 20) ? 4 : 1);
+    const int nb_target = rmgpu::tune("host_bands", rb * (size_t)H >= ((size_t)8 << 20) ? 6 : 1);
     const int R = std::max({halo, 64, (H + nb_target - 1) / std::max(1, nb_target)});
     const int nb = (H + R - 1) / R;
     if (nb < 2) {
