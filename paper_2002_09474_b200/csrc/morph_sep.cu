@@ -58,10 +58,12 @@ bool choose_b(int elem, int g, int* B_out) {
 bool choose_c(int elem, int g, int* C_out) {
     // (u16 with 16-column chunks -- 32 bytes per row per lane -- measured slower on cfg4: 377 vs
     // 408 Gpix/s)
+    // u8 wings 4..7 also take 16-column chunks: the windows inside a lane's chunk come from
+    // half-chunk scans (h_lane_pass)
     int C;
-    if (elem == 1) C = g >= 8 ? 16 : 8;
+    if (elem == 1) C = (g >= 8 || env_int("sep_c16_short", 1)) ? 16 : 8;
     else C = 8;
-    if (g < C / 2) return false;
+    if (g < 4 || (C == 8 && g < C / 2)) return false;
     const int A = g / C + (g % C ? 1 : 0);
     if (A > 8) return false;
     *C_out = C;
@@ -143,8 +145,11 @@ cudaError_t launch_v(const SepParams& p, int elem, int mode, int B, dim3 grid, c
     return mode == MODE_MIN ? launch_v_b<uint16_t, MODE_MIN>(p, B, grid, s, j) : launch_v_b<uint16_t, MODE_MAX>(p, B, grid, s, j);
 }
 
+// template code: g mod C, + 32 for the short-wing variant (the window fits in one chunk)
+int bx_code(int g, int C) { return g % C + (g < C && 2 * (g % C) < C ? 32 : 0); }
+
 cudaError_t launch_h(const SepParams& p, int elem, int mode, int C, dim3 grid, cudaStream_t s) {
-    const int bx = p.g % C;
+    const int bx = bx_code(p.g, C);
     if (elem == 1) return mode == MODE_MIN ? launch_h_u8_min(p, C, bx, grid, s) : launch_h_u8_max(p, C, bx, grid, s);
     return mode == MODE_MIN ? launch_h_u16_min(p, C, bx, grid, s) : launch_h_u16_max(p, C, bx, grid, s);
 }
@@ -235,7 +240,7 @@ cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int
     const long long warps = rowsw * p.parts;
     const dim3 grid((unsigned)((warps + HT / 32 - 1) / (HT / 32)));
     if (stages == 2) {
-        const int bx = p.g % C;
+        const int bx = bx_code(p.g, C);
         if (j.elem == 1) return j.mode == MODE_MIN ? launch_hh_u8_min(p, C, bx, grid, j.stream) : launch_hh_u8_max(p, C, bx, grid, j.stream);
         return j.mode == MODE_MIN ? launch_hh_u16_min(p, C, bx, grid, j.stream) : launch_hh_u16_max(p, C, bx, grid, j.stream);
     }

@@ -612,16 +612,47 @@ __device__ __forceinline__ uint2 shdn(uint2 v, int d) {
 // (compile-time). The next segment's rows are loaded before the current one is reduced.
 // One lane-chunk van Herk pass over the columns of a segment: x = this lane's C columns (4 rows
 // each), o = the window result for those columns (valid where the window's chunks are loaded).
-template <int MODE, int C, int BX>
+// BXS = g mod C, plus 32 for the short-wing variant (a = 0 and 2 (g mod C) < C: some windows
+// lie inside this lane's chunk; the planner picks it only when the wing is that short).
+template <int MODE, int C, int BXS>
 __device__ __forceinline__ void h_lane_pass(const uint2 (&x)[C], int a, uint2 (&o)[C]) {
     const uint2 ID = ident2<MODE>();
+    constexpr int BX = BXS & 31;
+    constexpr bool SHORT = BXS >= 32;
+    constexpr int HC = C / 2;
     uint2 P[C], S[C];
-    P[0] = x[0];
+    if constexpr (SHORT) {
+        // half-chunk scans: prefix / suffix within each half, then the chunk-wide ones from them;
+        // a window inside the chunk (2*BX+1 > C/2 columns) straddles the halves, so it is the left
+        // half's suffix joined with the right half's prefix (stored in o now, merged below)
+        P[0] = x[0];
+        P[HC] = x[HC];
+        S[HC - 1] = x[HC - 1];
+        S[C - 1] = x[C - 1];
 #pragma unroll
-    for (int c = 1; c < C; ++c) P[c] = op2<MODE>(P[c - 1], x[c]);
-    S[C - 1] = x[C - 1];
+        for (int c = 1; c < HC; ++c) {
+            P[c] = op2<MODE>(P[c - 1], x[c]);
+            P[HC + c] = op2<MODE>(P[HC + c - 1], x[HC + c]);
+        }
 #pragma unroll
-    for (int c = C - 2; c >= 0; --c) S[c] = op2<MODE>(S[c + 1], x[c]);
+        for (int c = HC - 2; c >= 0; --c) {
+            S[c] = op2<MODE>(S[c + 1], x[c]);
+            S[HC + c] = op2<MODE>(S[HC + c + 1], x[HC + c]);
+        }
+#pragma unroll
+        for (int j = BX; j < C - BX; ++j) o[j] = op2<MODE>(S[j - BX], P[j + BX]);  // in-chunk windows
+#pragma unroll
+        for (int c = HC; c < C; ++c) P[c] = op2<MODE>(P[HC - 1], P[c]);
+#pragma unroll
+        for (int c = 0; c < HC; ++c) S[c] = op2<MODE>(S[c], S[HC]);
+    } else {
+        P[0] = x[0];
+#pragma unroll
+        for (int c = 1; c < C; ++c) P[c] = op2<MODE>(P[c - 1], x[c]);
+        S[C - 1] = x[C - 1];
+#pragma unroll
+        for (int c = C - 2; c >= 0; --c) S[c] = op2<MODE>(S[c + 1], x[c]);
+    }
     const uint2 cm = P[C - 1];
     // chunk minima strictly inside the window: lanes L-a+1 .. L+a-1, plus lane L-a when the
     // left end lies one chunk further out (dl) and lane L+a when the right end does (dr)
@@ -645,7 +676,7 @@ __device__ __forceinline__ void h_lane_pass(const uint2 (&x)[C], int a, uint2 (&
         const uint2 sl = shup(S[(j - BX + C) % C], a + (dl ? 1 : 0));
         const uint2 pr = shdn(P[(j + BX) % C], a + (dr ? 1 : 0));
         const uint2 mid = dl ? (dr ? m11 : m10) : (dr ? m01 : m00);
-        o[j] = op3<MODE>(sl, mid, pr);
+        if (!(SHORT && !dl && !dr)) o[j] = op3<MODE>(sl, mid, pr);  // (else: in-chunk, kept)
     }
 }
 
@@ -682,7 +713,7 @@ __device__ __forceinline__ void h_border_fix(uint2 (&o)[C], int X, int cx, int H
 // (compile-time). The next segment's rows are loaded before the current one is reduced.
 // STAGES = 2: the two horizontal passes of an opening (MODE = min, then max) or closing in one
 // sweep -- the first pass's result never leaves registers; halo lanes double.
-template <typename T, int MODE, int C, int BX, int STAGES = 1>
+template <typename T, int MODE, int C, int BXS, int STAGES = 1>
 __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0, size_t sp, uint8_t* drow0,
                                        int nrows, int part) {
     using HC = HChunk<T, C>;
@@ -690,6 +721,7 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
     constexpr int MODE2 = MODE == MODE_MIN ? MODE_MAX : MODE_MIN;
     const int lane = threadIdx.x & 31;
     const int a = p.g / C;                   // whole chunks in the wing
+    constexpr int BX = BXS & 31;
     const int A = a + (BX > 0 ? 1 : 0);      // halo lanes on each side, per pass
     const int HA = STAGES * A;
     const int OS = (32 - 2 * HA) * C;        // output columns per segment
@@ -721,10 +753,10 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
         h_transpose_in<T, C>(q0, q1, q2, q3, x);
         if (Xn < xhi) load_seg(Xn, q0, q1, q2, q3);
         uint2 o[C];
-        h_lane_pass<MODE, C, BX>(x, a, o);
+        h_lane_pass<MODE, C, BXS>(x, a, o);
         if constexpr (STAGES == 2) {
             h_border_fix<T, C>(o, X, cx, HA, W, p.cmode, p.bval);
-            h_lane_pass<MODE2, C, BX>(o, a, x);
+            h_lane_pass<MODE2, C, BXS>(o, a, x);
 #pragma unroll
             for (int k = 0; k < C; ++k) o[k] = x[k];
         }
@@ -780,7 +812,7 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
 
 // One warp per (4-row group, column part).
 template <typename T, int MODE, int C, int BX, int STAGES = 1>
-__global__ void __launch_bounds__(HT) hpass_kernel(const SepParams p) {
+__global__ void __launch_bounds__(HT, STAGES == 1 ? 4 : 1) hpass_kernel(const SepParams p) {
     const int widx = blockIdx.x * (HT / 32) + (threadIdx.x >> 5);
     const int gidx = widx / p.parts;
     const int part = widx - gidx * p.parts;

@@ -288,6 +288,7 @@ SEP_KNOBS = [
     {"sep_pdl": 1},                       # PDL between the passes, H first
     {"sep_hh": 0},                        # opening / closing as four passes
     {"sep_hh": 2},                        # opening / closing always in three (also 16-column chunks)
+    {"sep_c16_short": 0},                 # u8 wings 4..7 in 8-column chunks (else half-chunk scans)
     {"sep_strip": 0},                     # H first into a row-major intermediate (not strip-major)
     {"sep_vbulk": 1, "sep_pf": 2},        # strip-major intermediate read by 1-D bulk copies (TMA pipeline)
 ]
