@@ -191,7 +191,9 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl 
     // the band is at least as tall as its warm-up (q-1 blocks): 4096^2 101x101 20.5 vs 21.6 us at
     // 40 rows, 63x63 flat; a 2(q-1)B floor was slower (fewer warps)
     const bool piped = sstride ? v_wants_bulk(j) : v_wants_tma(j);  // TMA pipeline vs plain loads
-    if (!piped) rb = std::min(rb, 80);  // plain loads: short bands (8192^2 63x63: rb 80 60.7 us, 160 64.2)
+    // plain loads: short bands (8192^2 63x63: rb 80 60.7 us, 160 64.2; cfg4's 1024-row images too:
+    // 423 vs 406 Gpix/s with whole-image bands)
+    if (!piped) rb = std::min(rb, 80);
     rb = std::max(rb, (p.q - 1) * B);
     // TMA path: bands of 320-640 rows (32768^2 63x63: rb 640 865 us, 160 895 us, one band per warp
     // per 2341 rows 1081 us)

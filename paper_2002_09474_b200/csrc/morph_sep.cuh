@@ -812,7 +812,7 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
 
 // One warp per (4-row group, column part).
 template <typename T, int MODE, int C, int BX, int STAGES = 1>
-__global__ void __launch_bounds__(HT, STAGES == 1 ? 4 : 1) hpass_kernel(const SepParams p) {
+__global__ void __launch_bounds__(HT, STAGES == 1 ? 4 : (C == 8 ? 5 : 2)) hpass_kernel(const SepParams p) {
     const int widx = blockIdx.x * (HT / 32) + (threadIdx.x >> 5);
     const int gidx = widx / p.parts;
     const int part = widx - gidx * p.parts;
