@@ -11,7 +11,7 @@ One step = those 16 operations. value = output Gpixel/s of the whole job (all ra
 Inputs are resident in HBM before the timed region; every operation of a step reads a different
 input copy and writes a different output buffer out of 32 rotating pairs (1 GiB total, > 8x the
 126 MB L2), so no operation is served from L2 by its predecessor. A step is one CUDA graph; its 16
-operations are independent, so the graph forks them over --streams (default 3) streams and one
+operations are independent, so the graph forks them over --streams (default 2) streams and one
 kernel's ramp-up / tail overlaps its neighbours. Per-window numbers ("per_window") are measured
 separately, one operation at a time. Device time is measured with CUDA events on the launching
 stream; multi-GPU time is the max over ranks.
@@ -55,7 +55,7 @@ def parse_args(argv=None):
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--eager", action="store_true", help="launch each op from Python instead of a CUDA graph")
-    p.add_argument("--streams", type=int, default=3,
+    p.add_argument("--streams", type=int, default=2,
                    help="streams the step graph forks its independent operations over (1 = serial)")
     p.add_argument("--soak-seconds", type=float, default=1.5)
     return p.parse_args(argv)
