@@ -299,15 +299,18 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
 
 // Measured (4096^2 / 16384^2 u8 1x63): 4 resident CTAs (<= 128 registers, small spills on the
 // border path) with the leading loads issued after the trailing suffix beat 3 CTAs with every load
-// hoisted: 12.4 vs 13-16 us, 65.5% vs 52-62% of HBM.
+// hoisted: 12.4 vs 13-16 us, 65.5% vs 52-62% of HBM. u8 blocks of <= 14 rows fit 6 CTAs (85
+// registers; one wave of the ~24-warps-per-SM band plan): 4096^2 1x31 12.1 -> 10.7 us, 31x31 17.7 ->
+// 16.6, 15x15 16.9 -> 16.5; taller blocks lose at 5-6 CTAs (101x101 B20 21.0 -> 23.1 us), and so
+// does u16 (cfg4 424 -> 417 Gpix/s).
 #ifndef SEP_VMINB
-#define SEP_VMINB 4
+#define SEP_VMINB(T, B) (sizeof(T) == 1 && (B) <= 14 ? 6 : 4)
 #endif
 #ifndef SEP_VHOIST
 #define SEP_VSPLIT 1
 #endif
 template <typename T, int MODE, int B, int QM, int SPC = 0>
-__global__ void __launch_bounds__(VT, SEP_VMINB) vpass_kernel(const SepParams p) {
+__global__ void __launch_bounds__(VT, SEP_VMINB(T, B)) vpass_kernel(const SepParams p) {
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // a dependent may start scheduling
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // no-op unless launched as a PDL dependent
     const int c = blockIdx.x * VT + threadIdx.x;
