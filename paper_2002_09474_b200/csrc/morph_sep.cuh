@@ -814,8 +814,15 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
 }
 
 // One warp per (4-row group, column part).
+// Resident CTAs per SM (4 warps each): one sweep, u8 16-column chunks need ~128 registers (5-6 CTAs
+// spill: 4096^2 63x63 19.1 -> 20.4 / 22.6 us); u16 8-column chunks fit 6 (4096^2 21x21 27.3 -> 24.8 us).
+#ifndef SEP_HMINB2C8
+#define SEP_HMINB2C8 5
+#endif
+#define SEP_HMINB(T, C, STAGES) \
+    ((STAGES) == 1 ? (sizeof(T) == 2 ? 6 : 4) : ((C) == 8 ? SEP_HMINB2C8 : 2))
 template <typename T, int MODE, int C, int BX, int STAGES = 1>
-__global__ void __launch_bounds__(HT, STAGES == 1 ? 4 : (C == 8 ? 5 : 2)) hpass_kernel(const SepParams p) {
+__global__ void __launch_bounds__(HT, SEP_HMINB(T, C, STAGES)) hpass_kernel(const SepParams p) {
     const int widx = blockIdx.x * (HT / 32) + (threadIdx.x >> 5);
     const int gidx = widx / p.parts;
     const int part = widx - gidx * p.parts;
