@@ -304,7 +304,10 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
 // 16.6, 15x15 16.9 -> 16.5; taller blocks lose at 5-6 CTAs (101x101 B20 21.0 -> 23.1 us), and so
 // does u16 (cfg4 424 -> 417 Gpix/s).
 #ifndef SEP_VMINB
-#define SEP_VMINB(T, B) (sizeof(T) == 1 && (B) <= 14 ? 6 : 4)
+#ifndef SEP_VMINB16
+#define SEP_VMINB16 4
+#endif
+#define SEP_VMINB(T, B) (sizeof(T) == 1 ? ((B) <= 14 ? 6 : 4) : SEP_VMINB16)
 #endif
 #ifndef SEP_VHOIST
 #define SEP_VSPLIT 1
@@ -819,10 +822,13 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
 #ifndef SEP_HMINB2C8
 #define SEP_HMINB2C8 5
 #endif
-#define SEP_HMINB(T, C, STAGES) \
-    ((STAGES) == 1 ? (sizeof(T) == 2 ? 6 : 4) : ((C) == 8 ? SEP_HMINB2C8 : 2))
+#ifndef SEP_HMINB_SHORT
+#define SEP_HMINB_SHORT 4
+#endif
+#define SEP_HMINB(T, C, BX, STAGES) \
+    ((STAGES) == 1 ? (sizeof(T) == 2 ? 6 : ((BX) >= 32 ? SEP_HMINB_SHORT : 4)) : ((C) == 8 ? SEP_HMINB2C8 : 2))
 template <typename T, int MODE, int C, int BX, int STAGES = 1>
-__global__ void __launch_bounds__(HT, SEP_HMINB(T, C, STAGES)) hpass_kernel(const SepParams p) {
+__global__ void __launch_bounds__(HT, SEP_HMINB(T, C, BX, STAGES)) hpass_kernel(const SepParams p) {
     const int widx = blockIdx.x * (HT / 32) + (threadIdx.x >> 5);
     const int gidx = widx / p.parts;
     const int part = widx - gidx * p.parts;
