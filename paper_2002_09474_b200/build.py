@@ -34,7 +34,9 @@ CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_fast.cu", "morph_fast_u8_min
               "morph_col_u16_max.cu", "morph_col_u8_grad.cu", "morph_col_u16_grad.cu", "morph_sep.cu",
               "morph_sep_h_u8_min.cu", "morph_sep_h_u8_max.cu", "morph_sep_h_u16_min.cu", "morph_sep_h_u16_max.cu",
               "transpose.cu",
-              "generate.cu"]
+              "generate.cu", "morph_fuse.cu"]
+# K4 instantiations: morph_fuse_inst.cu compiled once per (pixel size, mode, block size B)
+FUSE_VARIANTS = [(sz, mx, b) for sz in (1, 2) for mx in (0, 1) for b in ((8, 12, 16, 20, 24) if sz == 1 else (8, 12, 16))]
 HOST_SOURCES = [os.path.join("host", "rectmorph_b200.cpp")]
 
 
@@ -93,6 +95,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
         if force or _newer(o, [s] + sorted(_deps(s))):
             jobs.append([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o])
+    fsrc = os.path.join(CSRC, "morph_fuse_inst.cu")
+    fdeps = [fsrc] + sorted(_deps(fsrc))
+    for sz, mx, b in FUSE_VARIANTS:
+        o = os.path.join(OBJ, f"morph_fuse_u{8 * sz}_{'max' if mx else 'min'}_b{b}.o")
+        objs.append(o)
+        if force or _newer(o, fdeps):
+            jobs.append([NVCC] + NVCC_FLAGS + [f"-DFUSE_SZ={sz}", f"-DFUSE_MAX={mx}", f"-DFUSE_B={b}", "-c", fsrc, "-o", o])
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(_run, jobs))
     if force or jobs or _newer(LIB, objs):

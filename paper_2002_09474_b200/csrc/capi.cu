@@ -237,6 +237,10 @@ int run_single(MorphJob j) {
         if (e != cudaSuccess) return cuda_fail(e, "phase morph kernel");
         return RMGPU_OK;
     }
+    if (!g_disable_stream && rmgpu::fuse::launch(j, &e)) {
+        if (e != cudaSuccess) return cuda_fail(e, "fused separable kernel");
+        return RMGPU_OK;
+    }
     if (!g_disable_stream && rmgpu::sep::applicable(j)) {
         const size_t tb = rmgpu::sep::scratch_bytes(j);
         void* tmp = nullptr;
@@ -609,6 +613,8 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
         if (const char* n = rmgpu::col::plan_name(j)) return n;
     if (!g_disable_stream && j.elem == 2 && rmgpu::tune("u16_phase_first", 0))
         if (const char* n = rmgpu::phase::plan_name(j)) return n;
+    if (!g_disable_stream)
+        if (const char* n = rmgpu::fuse::plan_name(j)) return n;
     if (!g_disable_stream)
         if (const char* n = rmgpu::sep::plan_name(j)) return n;
     if (!g_disable_stream)

@@ -79,6 +79,12 @@ size_t compound_scratch_bytes(const MorphJob& j);
 cudaError_t run_compound(const MorphJob& j, void* tmp);
 }  // namespace sep
 
+// ---- K4: the separable rectangle in one kernel, intermediate in shared memory (morph_fuse.cu) ----
+namespace fuse {
+bool launch(const MorphJob& j, cudaError_t* err);  // false: K4 does not take this job
+const char* plan_name(const MorphJob& j);
+}  // namespace fuse
+
 // ---- transposes (transpose.cu) ---------------------------------------------------------------
 cudaError_t launch_transpose(const void* src, size_t sp, void* dst, size_t dp, int W, int H,
                              int elem, cudaStream_t s);
