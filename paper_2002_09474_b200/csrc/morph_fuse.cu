@@ -43,7 +43,7 @@ constexpr int kSmemPerSm = 228 * 1024;  // B200: shared memory per SM (1 KB rese
 
 struct Plan {
     int B = 0, q = 0, r = 0, C = 0, a = 0, A = 0, SW = 0, bxs = 0;
-    int NS = 0, PF = 0, nt = 0, smem = 0, ctas = 0;  // ctas: resident CTAs per SM the smem allows
+    int NS = 0, PF = 0, nt = 0, pair = 0, smem = 0, ctas = 0;  // ctas: resident CTAs per SM the smem allows
     int nstrips = 0, nb = 0, extra = 0, rba = 0, rbb = 0, per_img = 0;
     int ring_off = 0, tile_off = 0, bar_off = 0;
 };
@@ -52,7 +52,7 @@ int smem_bytes(int B, int r, int NS, int nt, int* ring_off, int* tile_off, int* 
     *ring_off = (r * RP + 127) / 128 * 128;  // guard rows in front of slot 0
     *tile_off = *ring_off + NS * B * RP;
     *bar_off = *tile_off + nt * B * RP;
-    return *bar_off + 8 * (2 * NS + 2 * NTMAX);
+    return *bar_off + 8 * (2 * NS + 2 * NTMAX);  // full (<= NS), tile full / empty, ring release
 }
 
 bool aligned(const MorphJob& j) {
@@ -61,7 +61,10 @@ bool aligned(const MorphJob& j) {
 }
 
 bool plan(const MorphJob& j, Plan* pl) {
-    if (!tune("fuse", 1)) return false;
+    // Off by default: measured against K3 (two launches through L2) it is still slower at 4096^2
+    // (63x63: 21.3 vs 18.7 us) and at 32768^2 (823 vs 789 us) -- both passes are latency / issue
+    // bound, not HBM bound, so removing the intermediate's traffic does not pay yet (K4).
+    if (!tune("fuse", 0)) return false;
     if (j.mode != MODE_MIN && j.mode != MODE_MAX) return false;
     if (j.elem != 1 && j.elem != 2) return false;
     if (j.W < 1 || j.H < 1 || j.batch < 1) return false;
@@ -80,10 +83,11 @@ bool plan(const MorphJob& j, Plan* pl) {
     // the vertical thread pays ~(2r + 30) / B for the tail fold, the block-minima fold and the
     // per-block synchronisation; PF >= 2 blocks of TMA prefetch when they fit next to a second CTA
     const int forced_b = tune("fuse_b", 0);
-    const int want_pf = tune("fuse_pf", 2);
-    const int smem_cap = kSmemPerSm / std::max(1, tune("fuse_ctas", 2)) - 1024;  // resident CTAs per SM
+    const int want_pf = tune("fuse_pf", FT > 256 ? 4 : 2);
+    const int smem_cap = kSmemPerSm / std::max(1, tune("fuse_ctas", FT > 256 ? 1 : 2)) - 1024;  // resident CTAs per SM
     double best = 1e30;
-    const int want_nt = tune("fuse_nt", 4);
+    const int want_nt = tune("fuse_nt", FT > 256 ? 8 : 4);
+    const int pair = std::min(2, std::max(1, tune("fuse_pair", 2)));
     for (int B : kB) {
         if (j.elem == 2 && B > 16) continue;
         if (forced_b && B != forced_b) continue;
@@ -95,7 +99,7 @@ bool plan(const MorphJob& j, Plan* pl) {
         bool done = false;
         for (int nt = std::min(want_nt, NTMAX); nt >= 2 && !done; nt /= 2) {
             for (int PF = std::max(1, want_pf); PF >= 1; --PF) {
-                const int NS = QQ + 1 + PF;
+                const int NS = (QQ + pair + PF + pair - 1) / pair * pair;
                 int ro, to, bo;
                 const int sm = smem_bytes(B, r, NS, nt, &ro, &to, &bo);
                 if (sm > smem_cap) continue;
@@ -107,6 +111,7 @@ bool plan(const MorphJob& j, Plan* pl) {
                     p.r = r;
                     p.PF = PF;
                     p.NS = NS;
+                    p.pair = pair;
                     p.nt = nt;
                     p.smem = sm;
                     p.ring_off = ro;
@@ -119,7 +124,7 @@ bool plan(const MorphJob& j, Plan* pl) {
         }
     }
     if (!p.B) return false;
-    p.ctas = std::max(1, std::min(2, kSmemPerSm / (p.smem + 1024)));
+    p.ctas = std::max(1, std::min(FT > 256 ? 1 : 2, kSmemPerSm / (p.smem + 1024)));
     // items: strips x bands x images, one CTA each. P items per image: every strip gets nb bands and
     // the first `extra` strips one more, so that the grid fills whole waves of resident CTAs (each
     // CTA's time is its band height plus the warm-up: 2 gy rows read for block minima and trailing
@@ -188,7 +193,7 @@ bool launch(const MorphJob& j, cudaError_t* err) {
     Plan p;
     if (!plan(j, &p)) return false;
     CUtensorMap map, gmap;
-    if (!stream::encode_input_map(j, RP / 4, p.B, &map)) return false;
+    if (p.pair * p.B > 256 || !stream::encode_input_map(j, RP / 4, p.pair * p.B, &map)) return false;
     if (p.r > 0) {
         if (!stream::encode_input_map(j, RP / 4, p.r, &gmap)) return false;
     } else {
@@ -220,8 +225,9 @@ bool launch(const MorphJob& j, cudaError_t* err) {
     fp.cmode = j.cmode;
     fp.bval = j.bval;
     fp.NS = p.NS;
+    fp.pair = p.pair;
     fp.nt = p.nt;
-    fp.ntlog = p.nt == 4 ? 2 : 1;
+    fp.ntlog = p.nt == 8 ? 3 : p.nt == 4 ? 2 : 1;
     fp.dbg = tune("fuse_dbg", 0);
     fp.trace = stream::g_trace;
     fp.trace_cta = stream::g_trace_cta;

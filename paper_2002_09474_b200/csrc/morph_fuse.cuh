@@ -34,13 +34,19 @@
 namespace rmgpu {
 namespace fuse {
 
-constexpr int FT = 256;   // threads per CTA: warps 0-3 vertical, 4-7 horizontal
-constexpr int NVT = 128;  // vertical threads (one 4-byte column word each)
-constexpr int NHT = 128;  // horizontal threads
+// One CTA per SM: 4 vertical warps, 11 horizontal warps (the horizontal pass is the heavier one:
+// measured alone, 8 horizontal warps per SM ran 1.9x longer than 8 vertical warps) and the TMA
+// producer warp.
+#ifndef FUSE_HWARPS
+#define FUSE_HWARPS 11
+#endif
+constexpr int NVT = 128;                 // vertical threads (one 4-byte column word each)
+constexpr int NHT = 32 * FUSE_HWARPS;    // horizontal threads
+constexpr int FT = NVT + NHT + 32;       // warps 0-3 vertical, then horizontal, the last one TMA
 constexpr int RP = 512;   // shared-memory row pitch: one strip row with its halo (bytes)
 constexpr int QM = 8;     // whole-block minima kept in registers (q - 1 <= QM)
 constexpr int RMAXG = 8;  // tail rows r = 2g mod B (guard rows in front of slot 0)
-constexpr int NTMAX = 4;  // tile slots (p.nt = 2 or 4, as the shared memory allows)
+constexpr int NTMAX = 8;  // tile slots (p.nt = 2, 4 or 8, as the shared memory allows)
 
 struct FuseParams {
     uint8_t* dst;
@@ -55,9 +61,10 @@ struct FuseParams {
     int nstrips, nb, extra, rba, rbb, per_img, batch;
     int cmode;
     uint32_t bval;
-    int NS;               // ring block slots
+    int NS;               // ring block slots (a multiple of pair)
+    int pair;             // blocks per TMA box / full barrier (1 or 2): fewer, larger TMA issues
     int nt, ntlog;        // tile slots (a power of two) and its log2
-    int dbg;              // tuning only: 1 = skip the horizontal math, 2 = skip the vertical math
+    int dbg;              // tuning only: skip the math -- 1 horizontal, 2 vertical, 3 both
     long long* trace;     // debug timeline of CTA trace_cta (tools/trace_fuse.py), normally null
     int trace_cta;
     int ring_off, tile_off, bar_off;  // shared-memory layout (bytes)
@@ -108,19 +115,19 @@ struct FV<uint16_t> {
 
 // Wait for a phase with a suspend-time hint: the warp sleeps in the barrier unit instead of
 // spinning on try_wait (a polling warp takes issue slots from the ALU-bound warps beside it).
-__device__ __forceinline__ void mbar_sleep(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "RM_SWAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-        "@P1 bra RM_SDONE;\n"
-        "bra RM_SWAIT;\n"
-        "RM_SDONE:\n"
-        "}\n" ::"r"(stream::saddr(bar)),
-        "r"(parity), "r"(0x100000u)
-        : "memory");
-}
+// (a macro, so that profiles attribute each wait to its call site)
+#define mbar_sleep(bar, parity)                                                   \
+    asm volatile(                                                                 \
+        "{\n"                                                                     \
+        ".reg .pred P1;\n"                                                        \
+        "RM_SWAIT:\n"                                                             \
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"            \
+        "@P1 bra RM_SDONE;\n"                                                     \
+        "bra RM_SWAIT;\n"                                                         \
+        "RM_SDONE:\n"                                                             \
+        "}\n" ::"r"(stream::saddr(bar)),                                          \
+        "r"(parity), "r"(0x100000u)                                               \
+        : "memory")
 
 // G op= the n most recent whole-block minima M[0..n) (n warp-uniform, <= QM): one branch instead
 // of a select per register.
@@ -213,7 +220,7 @@ __device__ __forceinline__ void h_group(const unsigned char* trow, uint8_t* drow
 }
 
 #ifndef FUSE_MINB
-#define FUSE_MINB 2
+#define FUSE_MINB (FT > 256 ? 1 : 2)
 #endif
 
 template <typename T, int MODE, int B, int BXS>
@@ -253,7 +260,7 @@ __global__ void __launch_bounds__(FT, FUSE_MINB) fused_kernel(const FuseParams p
     const int kmin = -QQ;      // first block loaded (the oldest trailing block of output block 0)
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < NS / p.pair; ++s) mbar_init(&full[s], 1);
         for (int s = 0; s < p.nt; ++s) {
             mbar_init(&tfull[s], NVT);
             mbar_init(&tempty[s], NHT);
@@ -265,21 +272,24 @@ __global__ void __launch_bounds__(FT, FUSE_MINB) fused_kernel(const FuseParams p
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int xw = (x0 * sz - 16 * p.A) / 4;  // map x of the strip row's first word (may be < 0)
-    auto issue = [&](int k) {  // block k -> its ring slot (the last slot also fills the guard rows)
-        const int s = (k - kmin) % NS;
-        const bool g = r > 0 && s == NS - 1;
-        mbar_arrive_tx(&full[s], (uint32_t)((B + (g ? r : 0)) * RP));
-        const int row = i0 + k * B - p.row_lo;
-        tma_box(ring + (size_t)s * B * RP, &map, xw, row, img, &full[s]);
-        if (g) tma_box(ring - (size_t)r * RP, &gmap, xw, row + B - r, img, &full[s]);
+    const int pair = p.pair, NU = NS / pair;  // ring units: pair consecutive blocks, one TMA box
+    auto issue = [&](int u) {  // unit u (blocks kmin + u * pair ...) -> its ring unit (the last
+                               // unit also fills the guard rows)
+        const int su = u % NU;
+        const bool g = r > 0 && su == NU - 1;
+        mbar_arrive_tx(&full[su], (uint32_t)((pair * B + (g ? r : 0)) * RP));
+        const int row = i0 + (kmin + u * pair) * B - p.row_lo;
+        tma_box(ring + (size_t)su * pair * B * RP, &map, xw, row, img, &full[su]);
+        if (g) tma_box(ring - (size_t)r * RP, &gmap, xw, row + pair * B - r, img, &full[su]);
     };
+    const int nunits = (nblk - kmin + pair - 1) / pair;  // units covering blocks kmin .. nblk - 1
     if (warp < NVT / 32) {
         // ------------------------------ vertical ------------------------------
         const int t = threadIdx.x;
         const int wo = 4 * t;
         if (t == 0) {
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map) : "memory");
-            for (int k = kmin; k < kmin + NS && k < nblk; ++k) issue(k);
+            for (int u = 0; u < NU && u < nunits; ++u) issue(u);
         }
         long long* tr = (p.trace && blockIdx.x == (unsigned)p.trace_cta && t == 0) ? p.trace : nullptr;
         const V ID = F::template id<MODE>();
@@ -287,11 +297,11 @@ __global__ void __launch_bounds__(FT, FUSE_MINB) fused_kernel(const FuseParams p
         V M[QM];
 #pragma unroll
         for (int k = 0; k < QM; ++k) M[k] = ID;
-        int s = 0, par = 0;  // ring slot of block k and its phase parity
+        int s = 0, par = 0;  // ring slot of block k and the phase parity of its unit
         for (int k = kmin; k < nblk; ++k) {
             unsigned char* sb = ring + (size_t)s * B * RP;
             if (tr) tr[(k - kmin) * 8 + 0] = clock64();
-            mbar_sleep(&full[s], (uint32_t)par);
+            if (s % pair == 0) mbar_sleep(&full[s / pair], (uint32_t)par);
             if (tr) tr[(k - kmin) * 8 + 1] = clock64();
             const int rs = i0 + k * B;  // first input row of block k
             if (rs < p.row_lo || rs + B > p.row_hi) {
@@ -310,9 +320,13 @@ __global__ void __launch_bounds__(FT, FUSE_MINB) fused_kernel(const FuseParams p
             if (k >= -(q - 1)) {
                 const unsigned char* pl = sb + wo;
                 if (k < 0) {  // warm-up block: its minimum only
-                    V P = F::ld(pl);
+                    V P = F::ld(pl), P2 = F::ld(pl + (B / 2) * RP);  // two half chains
 #pragma unroll
-                    for (int m = 1; m < B; ++m) P = F::template op<MODE>(P, F::ld(pl + m * RP));
+                    for (int m = 1; m < B / 2; ++m) {
+                        P = F::template op<MODE>(P, F::ld(pl + m * RP));
+                        P2 = F::template op<MODE>(P2, F::ld(pl + (B / 2 + m) * RP));
+                    }
+                    P = F::template op<MODE>(P, P2);
 #pragma unroll
                     for (int kk = QM - 1; kk > 0; --kk) M[kk] = M[kk - 1];
                     M[0] = P;
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(FT, FUSE_MINB) fused_kernel(const FuseParams p
                     int sf = st - (r > 0);  // slot of block L - QQ, whose last reader this is
                     if (sf < 0) sf += NS;
                     const int ts = L & (p.nt - 1);
-                    if (p.dbg == 2) {
+                    if (p.dbg >= 2) {
                         mbar_arrive(&rempty[sf]);
                         if (L >= p.nt) mbar_sleep(&tempty[ts], (uint32_t)(((L >> p.ntlog) & 1) ^ 1));
                         mbar_arrive(&tfull[ts]);
@@ -332,18 +346,25 @@ __global__ void __launch_bounds__(FT, FUSE_MINB) fused_kernel(const FuseParams p
                         // when block L-q sits in slot 0. The trailing suffix and the leading prefix
                         // are independent chains: interleaved, combined once the tile slot is free.
                         const unsigned char* pt = ring + (size_t)st * B * RP - (size_t)r * RP + wo;
+                        // Each chain split at HB = B / 2 into two independent half chains (four
+                        // chains in flight): Tm is the full suffix for rows >= HB and the suffix
+                        // within the lower half below; Pm the full prefix below HB and the prefix
+                        // within the upper half above. The halves' missing parts (Tm[HB], Pm[HB-1])
+                        // are folded into G once per half instead of per row.
+                        constexpr int HB = B / 2;
                         V Tm[B], Pm[B];
-                        V acc = F::ld(pt + (B - 1) * RP);
-                        V P = F::ld(pl);
-                        Tm[B - 1] = acc;
-                        Pm[0] = P;
+                        Tm[B - 1] = F::ld(pt + (B - 1) * RP);
+                        Tm[HB - 1] = F::ld(pt + (HB - 1) * RP);
+                        Pm[0] = F::ld(pl);
+                        Pm[HB] = F::ld(pl + HB * RP);
 #pragma unroll
-                        for (int m = 1; m < B; ++m) {
-                            acc = F::template op<MODE>(acc, F::ld(pt + (B - 1 - m) * RP));
-                            Tm[B - 1 - m] = acc;
-                            P = F::template op<MODE>(P, F::ld(pl + m * RP));
-                            Pm[m] = P;
+                        for (int j = 1; j < HB; ++j) {
+                            Tm[B - 1 - j] = F::template op<MODE>(Tm[B - j], F::ld(pt + (B - 1 - j) * RP));
+                            Tm[HB - 1 - j] = F::template op<MODE>(Tm[HB - j], F::ld(pt + (HB - 1 - j) * RP));
+                            Pm[j] = F::template op<MODE>(Pm[j - 1], F::ld(pl + j * RP));
+                            Pm[HB + j] = F::template op<MODE>(Pm[HB + j - 1], F::ld(pl + (HB + j) * RP));
                         }
+                        const V P = F::template op<MODE>(Pm[HB - 1], Pm[B - 1]);  // the block's minimum
                         V G = ID;
 #pragma unroll
                         for (int tt = 0; tt < RMAXG; ++tt)
@@ -354,8 +375,10 @@ __global__ void __launch_bounds__(FT, FUSE_MINB) fused_kernel(const FuseParams p
                         if (L >= p.nt) mbar_sleep(&tempty[ts], (uint32_t)(((L >> p.ntlog) & 1) ^ 1));
                         if (tr) tr[(k - kmin) * 8 + 2] = clock64();
                         unsigned char* to = tile + (size_t)ts * B * RP + wo;
+                        const V GL = F::template op<MODE>(G, Tm[HB]), GU = F::template op<MODE>(G, Pm[HB - 1]);
 #pragma unroll
-                        for (int m = 0; m < B; ++m) F::st(to + m * RP, F::template op3<MODE>(Tm[m], G, Pm[m]));
+                        for (int m = 0; m < B; ++m)
+                            F::st(to + m * RP, F::template op3<MODE>(Tm[m], m < HB ? GL : GU, Pm[m]));
 #pragma unroll
                         for (int kk = QM - 1; kk > 0; --kk) M[kk] = M[kk - 1];
                         M[0] = P;
@@ -369,40 +392,34 @@ __global__ void __launch_bounds__(FT, FUSE_MINB) fused_kernel(const FuseParams p
                 par ^= 1;
             }
         }
+    } else if (warp == FT / 32 - 1) {
+        // ------------------------------ TMA producer ------------------------------
+        // One warp refills released ring units in order: unit u (blocks kmin + u * pair ...) into
+        // the ring blocks of unit u - NU, once the last of those (released in block order) is
+        // released. A TMA issue costs hundreds of cycles under load, so it has its own warp, off
+        // the vertical and horizontal warps. Issuing in order is also what makes the parity-only
+        // waits on the release barriers exact: the slot's previous phase (unit u - 2 NU) was
+        // released before unit u - NU could be issued. The whole warp waits; lane 0 issues.
+        if (lane == 0) {  // a descriptor's first fetch is slow: before it is needed
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map) : "memory");
+            if (r > 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&gmap) : "memory");
+        }
+        for (int u = NU; u < nunits; ++u) {
+            const int last = (u - NU + 1) * pair - 1;  // relative to kmin
+            mbar_sleep(&rempty[last % NS], (uint32_t)((last / NS) & 1));
+            if (lane == 0) issue(u);
+            __syncwarp();
+        }
     } else {
-        // ------------------------------ horizontal (and TMA producer) ------------------------------
+        // ------------------------------ horizontal ------------------------------
         const int hw = warp - NVT / 32;
         const int ngroups = (y1 - y0 + 3) / 4;
         uint8_t* dimg = p.dst + (size_t)img * p.dimg;
-        // Lane 0 of horizontal warp 0 refills released ring slots in order (block k + NS into the
-        // slot of block k) -- off the critical vertical warps: a TMA issue costs hundreds of cycles
-        // under load. It polls without blocking after every group and before every wait for a
-        // tile, and blocks only for the blocks the vertical warps need to produce that tile (slot
-        // released >= PF blocks earlier: the wait is short).
-        const bool producer = hw == 0;  // the whole warp polls (no divergence around waits), lane 0 issues
-        if (producer && lane == 0) {  // a descriptor's first fetch is slow: before it is needed
-            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map) : "memory");
-            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&gmap) : "memory");
-        }
-        int next_issue = kmin + NS;  // next block to issue
-        int islot = 0;               // its slot (= the slot of block next_issue - NS)
-        auto refill = [&](int need) {  // issue every block whose slot is free; block for those <= need
-            while (next_issue < nblk) {
-                const uint32_t ph = (uint32_t)(((next_issue - NS - kmin) / NS) & 1);
-                if (next_issue > need && !mbar_test(&rempty[islot], ph)) break;
-                mbar_sleep(&rempty[islot], ph);
-                if (lane == 0) issue(next_issue);
-                __syncwarp();
-                ++next_issue;
-                if (++islot == NS) islot = 0;
-            }
-        };
         // A warp releases a tile slot only after that block's full phase has completed (also for
         // blocks holding none of its groups): otherwise its release of block d + nt could be
         // counted in block d's phase while another warp still reads block d.
         int done = 0, waited = -1;
         auto wait_tile = [&](int L) {
-            if (producer) refill(L);
             mbar_sleep(&tfull[L & (p.nt - 1)], (uint32_t)((L >> p.ntlog) & 1));
             waited = L;
         };
@@ -422,11 +439,10 @@ __global__ void __launch_bounds__(FT, FUSE_MINB) fused_kernel(const FuseParams p
             if (tr) tr[(G / 4) * 4 + 1] = clock64();
             const unsigned char* trow = tile + (size_t)(L & (p.nt - 1)) * B * RP + (size_t)(4 * G - L * B) * RP;
             const int y = y0 + 4 * G;
-            if (p.dbg != 1)
+            if (p.dbg != 1 && p.dbg != 3)
                 h_group<T, MODE, BXS>(trow, dimg + (size_t)y * p.dp, p.dp, min(4, y1 - y), x0, p.a, p.A, p.W, p.cmode,
                                       p.bval);
             if (tr) tr[(G / 4) * 4 + 2] = clock64();
-            if (producer) refill(-1);
         }
         release_to(nblk);
     }

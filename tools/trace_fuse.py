@@ -32,3 +32,9 @@ for w in range(4):
         if max(v) == 0:
             continue
         print(f"   {g:3d} | " + " ".join(f"{(x - t0):6d}" if x else "     -" for x in v))
+print("refill (H warp 0) | test  tested  slept  issued")
+for n in range(12):
+    v = [t[1024 + 200 + n * 4 + k] for k in range(4)]
+    if max(v) == 0:
+        continue
+    print(f"   {n:3d} | " + " ".join(f"{(x - t0):6d}" if x else "     -" for x in v))
