@@ -149,6 +149,23 @@ struct DispatchConfig {
 
 PassAlgorithm resolve(PassAlgorithm algo, int window, Axis axis, const DispatchConfig& cfg = {});
 
+// Config text and files (reference dispatch.hpp:46-57): "threshold_h=<int>\nthreshold_v=<int>\n
+// source=paper|calibrated\n"; parse_config is the strict inverse (Errc::BadConfig), load / save
+// fail with Errc::IoError naming the path.
+std::string format_config(const DispatchConfig& cfg);
+DispatchConfig parse_config(const std::string& text);
+DispatchConfig load_config(const std::string& path);
+void save_config(const std::string& path, const DispatchConfig& cfg);
+
+// calibrate (reference dispatch.hpp:59-66) measured on the current GPU: per swept window and
+// axis, the direct sliding window against van Herk (median of `reps` CUDA-event timings); the
+// thresholds are the largest windows where direct still wins. Validation as the reference
+// (reps < 3 -> Errc::InsufficientReps; empty, even or non-ascending windows, extents < 1).
+// The operations below honour a config whose source is Calibrated (each axis's resolved
+// algorithm is passed to the GPU planner); the paper's ARM thresholds (source Paper) leave the
+// choice to the planner's built-in B200 crossover. Results never depend on either.
+DispatchConfig calibrate(int width, int height, const std::vector<int>& windows, int reps);
+
 Image erode(const Image& src, const StructuringElement& se, const BorderPolicy& border, const DispatchConfig& cfg = {});
 Image dilate(const Image& src, const StructuringElement& se, const BorderPolicy& border, const DispatchConfig& cfg = {});
 Image opening(const Image& src, const StructuringElement& se, const BorderPolicy& border, const DispatchConfig& cfg = {});

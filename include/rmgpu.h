@@ -16,6 +16,9 @@
  *   rmgpu_transpose_tiles_*  rectmorph::transpose_tile   transpose.hpp:36-38
  *                            (batched; one tile = n_tiles 1)
  *   rmgpu_resolve            rectmorph::resolve          dispatch.hpp:24-28
+ *   rmgpu_format_config /    rectmorph::format_config / parse_config
+ *   rmgpu_parse_config                                   dispatch.hpp:46-57
+ *   rmgpu_calibrate          rectmorph::calibrate        dispatch.hpp:59-66
  *
  * Semantics follow the reference exactly (bit-exact outputs):
  *   - structuring element wx x wy (wx = se.width along a row, wy = se.height),
@@ -26,9 +29,12 @@
  *     re-applied to the intermediate image (dispatch.cpp:48-56);
  *   - gradient = dilate(x) - erode(x) (dispatch.cpp:58-71);
  *   - algo_h / algo_v are the reference's PassAlgorithm hints (Auto / Linear /
- *     VanHerk). Results never depend on them (tests/test_dispatch.cpp:68-79);
- *     they are accepted for API parity and ignored by the GPU planner, which
- *     picks its own kernel per window size.
+ *     VanHerk). Results never depend on them (tests/test_dispatch.cpp:68-79).
+ *     Auto lets the planner pick its kernel per window size (its built-in
+ *     crossover is what rmgpu_calibrate measures on a B200); an explicit Linear
+ *     on an axis whose wing is >= 4 runs that axis as a direct sliding window
+ *     (the generic pass kernel), an explicit VanHerk is honoured where a van
+ *     Herk kernel exists (wing >= 4) and is the planner's own choice otherwise.
  *
  * Memory: unless an entry point says "host", pointers are DEVICE pointers and
  * the call is asynchronous on `stream` (a cudaStream_t passed as void*, NULL =
@@ -61,6 +67,8 @@ enum rmgpu_status {
     RMGPU_ERR_EVEN_EXTENT = 2,      /* Errc::EvenExtent */
     RMGPU_ERR_UNSUPPORTED_TILE = 3, /* Errc::UnsupportedTile */
     RMGPU_ERR_BAD_CONFIG = 8,       /* Errc::BadConfig */
+    RMGPU_ERR_INSUFFICIENT_REPS = 9, /* Errc::InsufficientReps */
+    RMGPU_ERR_IO = 10,              /* Errc::IoError */
     RMGPU_ERR_BAD_ARGUMENT = 11,    /* Errc::BadArgument */
     RMGPU_ERR_CUDA = 64,            /* CUDA runtime failure (message in rmgpu_last_error) */
     RMGPU_ERR_NO_DEVICE = 65,       /* no sm_100 device visible */
@@ -151,9 +159,30 @@ int rmgpu_pass_host_u8(int which, const void* host_src, size_t src_pitch, void* 
 int rmgpu_window_1d_host_u8(const void* in, size_t n, int window, int op, int border_mode,
                             unsigned border_value, int algo, void* out);
 
-/* ---- dispatch (dispatch.hpp:16-28) -------------------------------------------------------- */
+/* ---- dispatch (dispatch.hpp:16-66) -------------------------------------------------------- */
 /* Auto -> Linear iff window <= threshold of the axis, inclusive; explicit choices pass through. */
 int rmgpu_resolve(int algo, int window, int axis, int threshold_h, int threshold_v);
+
+enum rmgpu_threshold_source { RMGPU_SOURCE_PAPER = 0, RMGPU_SOURCE_CALIBRATED = 1 };
+/* Canonical three-line text "threshold_h=<int>\nthreshold_v=<int>\nsource=paper|calibrated\n"
+ * (format_config, dispatch.hpp:46-50). Writes at most `cap` bytes including the NUL; returns the
+ * text length (without the NUL), so a return >= cap means the buffer was too small. */
+int rmgpu_format_config(int threshold_h, int threshold_v, int source, char* buf, size_t cap);
+/* Strict inverse (parse_config, dispatch.hpp:52-55; grammar of dispatch.cpp:112-156): blank
+ * lines and '#' comment lines ignored, spaces around keys / values and a trailing CR trimmed;
+ * unknown keys, duplicates, a line without '=', thresholds that are not positive odd integers,
+ * a source other than paper / calibrated, and missing keys -> RMGPU_ERR_BAD_CONFIG with the
+ * offending line in rmgpu_last_error(). */
+int rmgpu_parse_config(const char* text, int* threshold_h, int* threshold_v, int* source);
+/* calibrate (dispatch.hpp:59-66, dispatch.cpp:180-248) on the current device: per swept window
+ * w (odd, strictly ascending) and per axis, the median over `reps` (>= 3) CUDA-event timings of
+ * the direct sliding window (Linear) against van Herk on a deterministic width x height u8
+ * image; each threshold = the largest swept w where Linear is not slower (1 when it never is).
+ * Where no van Herk kernel exists (wing < 4) Linear wins by default. Validation (before any GPU
+ * work) as the reference: extents < 1 or empty / even / non-ascending windows -> BAD_ARGUMENT /
+ * EVEN_EXTENT / ZERO_EXTENT, reps < 3 -> INSUFFICIENT_REPS. */
+int rmgpu_calibrate(int width, int height, const int* windows, int n_windows, int reps,
+                    int* threshold_h, int* threshold_v);
 
 /* ---- synthetic inputs: counter-based generator shared with the CPU oracle ----------------- */
 /* pixel i (row-major) = byte (i&7) [u8] / half (i&3) [u16] of

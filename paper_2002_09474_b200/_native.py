@@ -38,6 +38,9 @@ SIGNATURES = {
     "rmgpu_pass_host_u8": [_I, _P, _S, _P, _S, _I, _I, _I, _I, _I, _U, _I],
     "rmgpu_window_1d_host_u8": [_P, _S, _I, _I, _I, _U, _I, _P],
     "rmgpu_resolve": [_I, _I, _I, _I, _I],
+    "rmgpu_format_config": [_I, _I, _I, C.c_char_p, _S],
+    "rmgpu_parse_config": [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "rmgpu_calibrate": [_I, _I, C.POINTER(C.c_int), _I, _I, C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "rmgpu_generate_u8": [_P, _S, _I, _I, _U64, _U64, _P],
     "rmgpu_generate_u16": [_P, _S, _I, _I, _U64, _U64, _P],
     "rmgpu_abi_version": [],

@@ -148,6 +148,58 @@ def resolve(algo: PassAlgorithm, window: int, axis: Axis, cfg: DispatchConfig | 
     return PassAlgorithm(lib().rmgpu_resolve(int(algo), window, int(axis), cfg.threshold_h, cfg.threshold_v))
 
 
+def format_config(cfg: DispatchConfig) -> str:
+    """dispatch.hpp:46-50: "threshold_h=..\\nthreshold_v=..\\nsource=paper|calibrated\\n"."""
+    buf = C.create_string_buffer(96)
+    n = lib().rmgpu_format_config(cfg.threshold_h, cfg.threshold_v, 1 if cfg.source == "calibrated" else 0,
+                                  buf, len(buf))
+    return buf.value[:n].decode()
+
+
+def parse_config(text: str) -> DispatchConfig:
+    """Strict inverse of format_config (dispatch.hpp:52-55); Error(Errc.BadConfig) otherwise."""
+    th, tv, src = C.c_int(0), C.c_int(0), C.c_int(0)
+    _check(lib().rmgpu_parse_config(text.encode(), C.byref(th), C.byref(tv), C.byref(src)))
+    return DispatchConfig(th.value, tv.value, "calibrated" if src.value == 1 else "paper")
+
+
+def load_config(path: str) -> DispatchConfig:
+    try:
+        with open(path, "rb") as f:
+            text = f.read().decode(errors="replace")
+    except OSError:
+        raise Error(Errc.IoError, f"cannot open config '{path}'") from None
+    try:
+        return parse_config(text)
+    except Error as e:
+        raise Error(e.code, f"{path}: {e}") from None
+
+
+def save_config(path: str, cfg: DispatchConfig) -> None:
+    try:
+        with open(path, "wb") as f:
+            f.write(format_config(cfg).encode())
+    except OSError:
+        raise Error(Errc.IoError, f"cannot open '{path}' for writing") from None
+
+
+def calibrate(width: int, height: int, windows, reps: int) -> DispatchConfig:
+    """dispatch.hpp:59-66 measured on the current GPU (rmgpu_calibrate)."""
+    ws = list(windows)
+    arr = (C.c_int * max(1, len(ws)))(*ws)
+    th, tv = C.c_int(0), C.c_int(0)
+    _check(lib().rmgpu_calibrate(width, height, arr, len(ws), reps, C.byref(th), C.byref(tv)))
+    return DispatchConfig(th.value, tv.value, "calibrated")
+
+
+def _hints(se, cfg: DispatchConfig | None) -> tuple[int, int]:
+    """A Calibrated config steers the GPU planner axis by axis; the paper's thresholds do not."""
+    if cfg is None or cfg.source != "calibrated":
+        return 0, 0
+    return (int(resolve(PassAlgorithm.Auto, se.width, Axis.Horizontal, cfg)),
+            int(resolve(PassAlgorithm.Auto, se.height, Axis.Vertical, cfg)))
+
+
 # ------------------------------------------------------------------------------------------
 # host level
 # ------------------------------------------------------------------------------------------
@@ -158,42 +210,45 @@ def _host_image(img: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(img)
 
 
-def _morph_host(img: np.ndarray, se: StructuringElement, border: BorderPolicy, op: int) -> np.ndarray:
+def _morph_host(img: np.ndarray, se: StructuringElement, border: BorderPolicy, op: int,
+                hints: tuple[int, int] = (0, 0)) -> np.ndarray:
     img = _host_image(img)
     h, w = img.shape
     out = np.empty_like(img)
     es = img.itemsize
     fn = lib().rmgpu_morph_host_u8 if es == 1 else lib().rmgpu_morph_host_u16
     _check(fn(img.ctypes.data, w * es, out.ctypes.data, w * es, w, h, se.width, se.height, op,
-              border.mode, border.value, 0, 0))
+              border.mode, border.value, hints[0], hints[1]))
     return out
 
 
 def erode(img, se, border=BorderPolicy(), cfg=None):
-    return _morph_host(img, se, border, ERODE)
+    return _morph_host(img, se, border, ERODE, _hints(se, cfg))
 
 
 def dilate(img, se, border=BorderPolicy(), cfg=None):
-    return _morph_host(img, se, border, DILATE)
+    return _morph_host(img, se, border, DILATE, _hints(se, cfg))
 
 
 def opening(img, se, border=BorderPolicy(), cfg=None):
-    return _morph_host(img, se, border, OPEN)
+    return _morph_host(img, se, border, OPEN, _hints(se, cfg))
 
 
 def closing(img, se, border=BorderPolicy(), cfg=None):
-    return _morph_host(img, se, border, CLOSE)
+    return _morph_host(img, se, border, CLOSE, _hints(se, cfg))
 
 
 def gradient(img, se, border=BorderPolicy(), cfg=None):
-    return _morph_host(img, se, border, GRADIENT)
+    return _morph_host(img, se, border, GRADIENT, _hints(se, cfg))
 
 
 def morph_separable(img, op: OpKind, se, border=BorderPolicy(), h_algo=PassAlgorithm.Auto,
                     v_algo=PassAlgorithm.Auto, v_strategy=None):
     _validate_window(se.width)
     _validate_window(se.height)
-    return _morph_host(img, se, border, int(op))
+    # the explicit per-axis algorithms are GPU planner hints (rmgpu.h); v_strategy has no GPU
+    # counterpart (both strategies are the same fused column pass)
+    return _morph_host(img, se, border, int(op), (int(h_algo), int(v_algo)))
 
 
 def _pass(which: int, img, op: OpKind, window: int, border: BorderPolicy) -> np.ndarray:
@@ -298,6 +353,12 @@ def _dev(t):
     return t
 
 
+def _same(src, dst, what: str = "dst") -> None:
+    """dst must match src in dtype and device (and shape, checked by the callers)."""
+    if src.dtype != dst.dtype or src.device != dst.device:
+        raise Error(Errc.BadArgument, f"{what} must have the source's dtype and device")
+
+
 def _stream_ptr(stream):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -308,6 +369,9 @@ def morph_device(src, dst, wx: int, wy: int, op: int, border: int = REPLICATE, v
                  stream=None) -> None:
     """2-D tensors [H, W] (row pitch from stride(0)). Asynchronous on ``stream``."""
     _dev(src), _dev(dst)
+    _same(src, dst)
+    if src.dim() != 2 or tuple(dst.shape) != tuple(src.shape):
+        raise Error(Errc.BadArgument, "src and dst must be 2-D tensors of the same shape")
     h, w = src.shape
     es = src.element_size()
     fn = lib().rmgpu_morph_u8 if es == 1 else lib().rmgpu_morph_u16
@@ -318,6 +382,9 @@ def morph_device(src, dst, wx: int, wy: int, op: int, border: int = REPLICATE, v
 def morph_batched_device(src, dst, wx, wy, op, border=REPLICATE, value=0, stream=None) -> None:
     """3-D tensors [B, H, W]."""
     _dev(src), _dev(dst)
+    _same(src, dst)
+    if src.dim() != 3 or tuple(dst.shape) != tuple(src.shape):
+        raise Error(Errc.BadArgument, "src and dst must be 3-D tensors of the same shape")
     b, h, w = src.shape
     es = src.element_size()
     fn = lib().rmgpu_morph_batched_u8 if es == 1 else lib().rmgpu_morph_batched_u16
@@ -329,6 +396,11 @@ def morph_band_device(src_with_halo, rows_above: int, rows_below: int, dst, wx, 
                       value=0, stream=None) -> None:
     """``src_with_halo`` holds rows_above + band_rows + rows_below rows; dst holds band_rows."""
     _dev(src_with_halo), _dev(dst)
+    _same(src_with_halo, dst)
+    if src_with_halo.dim() != 2 or dst.dim() != 2 or src_with_halo.shape[1] != dst.shape[1]:
+        raise Error(Errc.BadArgument, "src_with_halo and dst must be 2-D tensors of the same width")
+    if rows_above < 0 or rows_below < 0 or src_with_halo.shape[0] < rows_above + dst.shape[0] + rows_below:
+        raise Error(Errc.BadArgument, "src_with_halo must hold rows_above + band rows + rows_below rows")
     rows, w = dst.shape
     es = dst.element_size()
     base = src_with_halo.data_ptr() + rows_above * src_with_halo.stride(0) * es
@@ -339,6 +411,9 @@ def morph_band_device(src_with_halo, rows_above: int, rows_below: int, dst, wx, 
 
 def transpose_device(src, dst, stream=None) -> None:
     _dev(src), _dev(dst)
+    _same(src, dst)
+    if src.dim() != 2 or tuple(dst.shape) != (src.shape[1], src.shape[0]):
+        raise Error(Errc.BadArgument, "dst must be the W x H transpose shape of src")
     h, w = src.shape
     es = src.element_size()
     fn = lib().rmgpu_transpose_u8 if es == 1 else lib().rmgpu_transpose_u16

@@ -155,15 +155,24 @@ int check_device() {
             msg = std::string("no CUDA device: ") + cudaGetErrorString(e);
             return;
         }
-        cudaDeviceProp p{};
-        cudaGetDeviceProperties(&p, 0);
-        if (p.major != 10) {
-            status = RMGPU_ERR_NO_DEVICE;
-            msg = "librmgpu is built for sm_100a only; device 0 is sm_" + std::to_string(p.major) +
-                  std::to_string(p.minor);
-        }
     });
     if (status != RMGPU_OK) return fail(status, msg);
+    // the architecture of the device the caller is using (cached per device)
+    static int arch_ok[64] = {};  // 0 unknown, 1 sm_100, 2 other
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(RMGPU_ERR_NO_DEVICE, "cudaGetDevice failed");
+    int ok = (dev >= 0 && dev < 64) ? __atomic_load_n(&arch_ok[dev], __ATOMIC_RELAXED) : 0;
+    int major = 0, minor = 0;
+    if (!ok) {
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        ok = major == 10 ? 1 : 2;
+        if (dev >= 0 && dev < 64) __atomic_store_n(&arch_ok[dev], ok, __ATOMIC_RELAXED);
+    }
+    if (ok != 1)
+        return fail(RMGPU_ERR_NO_DEVICE, "librmgpu is built for sm_100a only; device " + std::to_string(dev) +
+                                             " is not sm_100" + (major ? " (sm_" + std::to_string(major) +
+                                                                 std::to_string(minor) + ")" : std::string()));
     return RMGPU_OK;
 }
 
@@ -227,6 +236,49 @@ int run_single(MorphJob j) {
         return RMGPU_OK;
     }
     cudaError_t e = cudaSuccess;
+    // Explicit algorithm hints (rmgpu.h): Linear on an axis whose wing is >= 4 runs that axis as a
+    // direct sliding window (generic pass kernel), the other axis through the planner, via one
+    // intermediate; everything else (Auto, VanHerk, Linear on short wings -- where the planner's
+    // kernels are direct windows already) is the planner's choice. Results are identical.
+    const bool direct_h = j.algo_h == RMGPU_ALGO_LINEAR && j.gx >= 4;
+    const bool direct_v = j.algo_v == RMGPU_ALGO_LINEAR && j.gy >= 4;
+    if ((direct_h || direct_v) && j.mode != rmgpu::MODE_GRAD) {
+        const size_t tp = ((size_t)j.W * j.elem + 255) & ~size_t(255), timg = tp * (size_t)j.H;
+        void* tmp = nullptr;
+        if (j.gx && j.gy) RM_CUDA(scratch_alloc(&tmp, timg * j.batch, j.stream));
+        MorphJob v = j, h = j;
+        v.gx = 0;
+        v.algo_h = v.algo_v = RMGPU_ALGO_AUTO;
+        h.gy = 0;
+        h.algo_h = h.algo_v = RMGPU_ALGO_AUTO;
+        h.above = h.below = 0;
+        if (j.gx && j.gy) {
+            v.dst = tmp; v.dp = tp; v.dimg = timg;
+            h.src = tmp; h.sp = tp; h.simg = timg;
+        }
+        int rc = RMGPU_OK;
+        if (j.gy) {
+            if (direct_v) {
+                e = rmgpu::launch_pass_cols(v);
+                if (e != cudaSuccess) rc = cuda_fail(e, "direct vertical pass");
+            } else {
+                rc = run_single(v);
+            }
+        }
+        if (rc == RMGPU_OK && j.gx) {
+            if (direct_h) {
+                e = rmgpu::launch_pass_rows(h);
+                if (e != cudaSuccess) rc = cuda_fail(e, "direct horizontal pass");
+            } else {
+                rc = run_single(h);
+            }
+        }
+        if (tmp) {
+            cudaError_t fe = cudaFreeAsync(tmp, j.stream);
+            if (rc == RMGPU_OK && fe != cudaSuccess) rc = cuda_fail(fe, "cudaFreeAsync");
+        }
+        return rc;
+    }
     if (!g_disable_stream && rmgpu::col::launch(j, &e)) {
         if (e != cudaSuccess) return cuda_fail(e, "register-streaming morph kernel");
         return RMGPU_OK;
@@ -364,13 +416,21 @@ gradient_fallback:
 // Full op (erode/dilate/open/close/gradient) over a whole image, batch or row band.
 int run_morph(const void* src, size_t sp, size_t simg, void* dst, size_t dp, size_t dimg, int batch, int W,
               int H, int above, int below, int wx, int wy, int op, int border, unsigned bval, int elem,
-              cudaStream_t stream) {
+              cudaStream_t stream, int algo_h = RMGPU_ALGO_AUTO, int algo_v = RMGPU_ALGO_AUTO) {
     int rc;
     if ((rc = check_se(wx, wy))) return rc;
     if ((rc = check_op_border(op, border, bval, elem))) return rc;
     if ((rc = check_image(src, sp, dst, dp, W, H, elem))) return rc;
     if (above < 0 || below < 0 || batch < 0) return fail(RMGPU_ERR_BAD_ARGUMENT, "negative halo or batch");
     if (W == 0 || H == 0 || batch == 0) return RMGPU_OK;
+    {
+        // context rows past the ones a window can reach are never read (every valid tap of every
+        // output row is already inside [-reach, H + reach)): drop them, so a caller that passes a
+        // whole image as context pays only for the halo (compound ops reach two wings)
+        const int reach = (op == RMGPU_OPEN || op == RMGPU_CLOSE) ? 2 * (wy / 2) : wy / 2;
+        above = std::min(above, reach);
+        below = std::min(below, reach);
+    }
     if ((rc = check_device())) return rc;
 
     MorphJob j;
@@ -382,12 +442,17 @@ int run_morph(const void* src, size_t sp, size_t simg, void* dst, size_t dp, siz
     j.gy = std::min(wy / 2, H + above + below);
     j.cmode = border; j.bval = bval; j.elem = elem; j.batch = batch; j.simg = simg; j.dimg = dimg;
     j.stream = stream;
+    if (algo_h < RMGPU_ALGO_AUTO || algo_h > RMGPU_ALGO_VANHERK || algo_v < RMGPU_ALGO_AUTO ||
+        algo_v > RMGPU_ALGO_VANHERK)
+        return fail(RMGPU_ERR_BAD_ARGUMENT, "unknown pass algorithm");
+    j.algo_h = algo_h;
+    j.algo_v = algo_v;
 
     if (op == RMGPU_ERODE || op == RMGPU_DILATE || op == RMGPU_GRADIENT) {
         j.mode = op == RMGPU_ERODE ? rmgpu::MODE_MIN : op == RMGPU_DILATE ? rmgpu::MODE_MAX : rmgpu::MODE_GRAD;
         return run_single(j);
     }
-    if (!g_disable_stream && above == 0 && below == 0) {
+    if (!g_disable_stream && above == 0 && below == 0 && algo_h != RMGPU_ALGO_LINEAR && algo_v != RMGPU_ALGO_LINEAR) {
         MorphJob c = j;
         c.mode = op == RMGPU_OPEN ? rmgpu::MODE_MIN : rmgpu::MODE_MAX;
         if (rmgpu::sep::compound_applicable(c)) {
@@ -474,7 +539,7 @@ struct DevBuf {
 };
 
 int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int wx, int wy, int op,
-               int border, unsigned bval, int elem) {
+               int border, unsigned bval, int elem, int algo_h, int algo_v) {
     int rc;
     if ((rc = check_se(wx, wy))) return rc;
     if ((rc = check_op_border(op, border, bval, elem))) return rc;
@@ -501,7 +566,7 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     if (nb < 2) {
         if (sp == rb && pitch == rb) RM_CUDA(cudaMemcpyAsync(a.p, hsrc, rb * H, cudaMemcpyHostToDevice, s));
         else RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, rb, H, cudaMemcpyHostToDevice, s));
-        rc = run_morph(a.p, pitch, 0, b.p, pitch, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, elem, s);
+        rc = run_morph(a.p, pitch, 0, b.p, pitch, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, elem, s, algo_h, algo_v);
         if (rc) return rc;
         if (dp == rb && pitch == rb) RM_CUDA(cudaMemcpyAsync(hdst, b.p, rb * H, cudaMemcpyDeviceToHost, s));
         else RM_CUDA(cudaMemcpy2DAsync(hdst, dp, b.p, pitch, rb, H, cudaMemcpyDeviceToHost, s));
@@ -509,6 +574,18 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
         return RMGPU_OK;
     }
     if ((rc = host_events(2 * (size_t)nb + 1))) return rc;
+    // Any early return below leaves copies queued on `up` / `down` that still use a.p / b.p: this
+    // guard (destroyed before the DevBufs) waits for both copy streams first, so the buffers are
+    // never handed back to the pool while a copy can still touch them.
+    struct Drain {
+        bool armed = true;
+        ~Drain() {
+            if (armed) {
+                cudaStreamSynchronize(t_ctx.up);
+                cudaStreamSynchronize(t_ctx.down);
+            }
+        }
+    } drain;
     cudaEvent_t* ev_in = t_ctx.events.data();
     cudaEvent_t* ev_out = ev_in + nb;
     cudaEvent_t ev_start = ev_in[2 * nb];
@@ -531,7 +608,7 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
         const int above = std::min(halo, r0), below = std::min(halo, H - r0 - n);
         rc = run_morph(static_cast<char*>(a.p) + (size_t)r0 * pitch, pitch, 0,
                        static_cast<char*>(b.p) + (size_t)r0 * pitch, pitch, 0, 1, W, n, above, below, wx, wy, op,
-                       border, bval, elem, s);
+                       border, bval, elem, s, algo_h, algo_v);
         if (rc) return rc;
         RM_CUDA(cudaEventRecord(ev_out[k], s));
         RM_CUDA(cudaStreamWaitEvent(t_ctx.down, ev_out[k], 0));
@@ -542,7 +619,7 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     }
     RM_CUDA(cudaStreamSynchronize(t_ctx.down));
     RM_CUDA(cudaStreamSynchronize(s));
-    // the buffers are freed on `s` (DevBuf): every copy that used them has completed
+    drain.armed = false;  // the buffers are freed on `s` (DevBuf): every copy that used them has completed
     return RMGPU_OK;
 }
 
@@ -595,6 +672,163 @@ void rmgpu_debug_set(const char* knob, int value) {
     else rmgpu::g_tune[knob] = value;
 }
 
+int rmgpu_format_config(int threshold_h, int threshold_v, int source, char* buf, size_t cap) {
+    const std::string text = "threshold_h=" + std::to_string(threshold_h) + "\nthreshold_v=" +
+                             std::to_string(threshold_v) + "\nsource=" +
+                             (source == RMGPU_SOURCE_CALIBRATED ? "calibrated" : "paper") + "\n";
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, text.size());
+        memcpy(buf, text.data(), n);
+        buf[n] = 0;
+    }
+    return (int)text.size();
+}
+
+int rmgpu_parse_config(const char* text, int* threshold_h, int* threshold_v, int* source) {
+    if (!text) return fail(RMGPU_ERR_BAD_ARGUMENT, "null config text");
+    auto strip = [](std::string v) {
+        size_t a = 0, b = v.size();
+        while (a < b && (v[a] == ' ' || v[a] == '\t')) ++a;
+        while (b > a && (v[b - 1] == ' ' || v[b - 1] == '\t' || v[b - 1] == '\r')) --b;
+        return v.substr(a, b - a);
+    };
+    auto bad = [](int line, const std::string& what) {
+        return fail(RMGPU_ERR_BAD_CONFIG, "config line " + std::to_string(line) + ": " + what);
+    };
+    int th = 0, tv = 0, src = RMGPU_SOURCE_PAPER;
+    bool have_h = false, have_v = false, have_s = false;
+    const std::string all(text);
+    size_t pos = 0;
+    int line = 0;
+    while (pos <= all.size()) {
+        size_t nl = all.find('\n', pos);
+        if (nl == std::string::npos) nl = all.size();
+        const std::string ln = strip(all.substr(pos, nl - pos));
+        ++line;
+        pos = nl + 1;
+        if (ln.empty() || ln[0] == '#') {
+            if (nl == all.size()) break;
+            continue;
+        }
+        const size_t eq = ln.find('=');
+        if (eq == std::string::npos) return bad(line, "expected key=value");
+        const std::string key = strip(ln.substr(0, eq)), val = strip(ln.substr(eq + 1));
+        if (key == "threshold_h" || key == "threshold_v") {
+            bool& seen = key == "threshold_h" ? have_h : have_v;
+            if (seen) return bad(line, "duplicate key '" + key + "'");
+            // a whole decimal integer (optional sign), positive and odd
+            bool ok = !val.empty();
+            long long v = 0;
+            size_t i = (val[0] == '-' || val[0] == '+') ? 1 : 0;
+            if (i == val.size()) ok = false;
+            for (; ok && i < val.size(); ++i) {
+                if (val[i] < '0' || val[i] > '9') ok = false;
+                else if ((v = v * 10 + (val[i] - '0')) > 0x7fffffff) ok = false;
+            }
+            if (!ok) return bad(line, "expected an integer, got '" + val + "'");
+            if (val[0] == '-') v = -v;
+            if (v < 1 || v % 2 == 0) return bad(line, "threshold must be a positive odd integer");
+            (key == "threshold_h" ? th : tv) = (int)v;
+            seen = true;
+        } else if (key == "source") {
+            if (have_s) return bad(line, "duplicate key 'source'");
+            if (val == "paper") src = RMGPU_SOURCE_PAPER;
+            else if (val == "calibrated") src = RMGPU_SOURCE_CALIBRATED;
+            else return bad(line, "source must be 'paper' or 'calibrated'");
+            have_s = true;
+        } else {
+            return bad(line, "unknown key '" + key + "'");
+        }
+        if (nl == all.size()) break;
+    }
+    if (!have_h || !have_v || !have_s) return fail(RMGPU_ERR_BAD_CONFIG, "config must set threshold_h, threshold_v and source");
+    if (threshold_h) *threshold_h = th;
+    if (threshold_v) *threshold_v = tv;
+    if (source) *source = src;
+    return RMGPU_OK;
+}
+
+int rmgpu_calibrate(int width, int height, const int* windows, int n_windows, int reps, int* threshold_h,
+                    int* threshold_v) {
+    // validation in the reference's order (dispatch.cpp:182-194), before any device work
+    if (width < 1 || height < 1) return fail(RMGPU_ERR_BAD_ARGUMENT, "calibration image extents must be >= 1");
+    if (reps < 3) return fail(RMGPU_ERR_INSUFFICIENT_REPS, "calibration needs at least 3 repetitions");
+    if (n_windows < 1 || !windows) return fail(RMGPU_ERR_BAD_ARGUMENT, "calibration needs at least one window");
+    for (int i = 0; i < n_windows; ++i) {
+        int rc = check_window(windows[i]);
+        if (rc) return rc;
+        if (i > 0 && windows[i] <= windows[i - 1])
+            return fail(RMGPU_ERR_BAD_ARGUMENT, "calibration windows must be strictly ascending");
+    }
+    int rc = check_device();
+    if (rc) return rc;
+    cudaStream_t s = nullptr;
+    RM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    } sg{s};
+    const size_t pitch = ((size_t)width + 255) & ~size_t(255);
+    void *src = nullptr, *dst = nullptr;
+    RM_CUDA(cudaMallocAsync(&src, pitch * height, s));
+    RM_CUDA(cudaMallocAsync(&dst, pitch * height, s));
+    struct BufGuard {
+        void *a, *b;
+        cudaStream_t s;
+        ~BufGuard() { cudaFreeAsync(a, s); cudaFreeAsync(b, s); }
+    } bg{src, dst, s};
+    // deterministic pixels: repeated calibrations time identical data (dispatch.cpp:196-201)
+    RM_CUDA(rmgpu::launch_generate(src, pitch, width, height, 0x7261746Dull, 0, 1, s));
+    cudaEvent_t e0, e1;
+    RM_CUDA(cudaEventCreate(&e0));
+    RM_CUDA(cudaEventCreate(&e1));
+    struct EvGuard {
+        cudaEvent_t a, b;
+        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
+    } eg{e0, e1};
+    // median over reps of one pass (erosion, replicate) with the given axis / algorithm
+    auto median_ms = [&](int wx, int wy, int ah, int av, float* out) -> int {
+        std::vector<float> t;
+        for (int k = 0; k <= reps; ++k) {  // k = 0: warm-up (planner caches, first launch)
+            RM_CUDA(cudaEventRecord(e0, s));
+            int r = run_morph(src, pitch, 0, dst, pitch, 0, 1, width, height, 0, 0, wx, wy, RMGPU_ERODE,
+                              RMGPU_BORDER_REPLICATE, 0, 1, s, ah, av);
+            if (r) return r;
+            RM_CUDA(cudaEventRecord(e1, s));
+            RM_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            RM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            if (k) t.push_back(ms);
+        }
+        std::sort(t.begin(), t.end());
+        *out = t[t.size() / 2];
+        return RMGPU_OK;
+    };
+    int best_h = 1, best_v = 1;
+    for (int i = 0; i < n_windows; ++i) {
+        const int w = windows[i];
+        float lin = 0, vh = 0;
+        // horizontal pass: w x 1. Wings < 4 have no van Herk kernel: Linear wins by default.
+        if ((rc = median_ms(w, 1, RMGPU_ALGO_LINEAR, RMGPU_ALGO_AUTO, &lin))) return rc;
+        if (w / 2 >= 4) {
+            if ((rc = median_ms(w, 1, RMGPU_ALGO_VANHERK, RMGPU_ALGO_AUTO, &vh))) return rc;
+        } else {
+            vh = lin;
+        }
+        if (lin <= vh) best_h = std::max(best_h, w);
+        if ((rc = median_ms(1, w, RMGPU_ALGO_AUTO, RMGPU_ALGO_LINEAR, &lin))) return rc;
+        if (w / 2 >= 4) {
+            if ((rc = median_ms(1, w, RMGPU_ALGO_AUTO, RMGPU_ALGO_VANHERK, &vh))) return rc;
+        } else {
+            vh = lin;
+        }
+        if (lin <= vh) best_v = std::max(best_v, w);
+    }
+    if (threshold_h) *threshold_h = best_h;
+    if (threshold_v) *threshold_v = best_v;
+    return RMGPU_OK;
+}
+
 int rmgpu_resolve(int algo, int window, int axis, int threshold_h, int threshold_v) {
     if (algo != RMGPU_ALGO_AUTO) return algo;  // dispatch.cpp:14-20
     const int t = axis == RMGPU_AXIS_HORIZONTAL ? threshold_h : threshold_v;
@@ -638,9 +872,8 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
 #define MORPH_ENTRY(SFX, ELEM)                                                                          \
     int rmgpu_morph_##SFX(const void* src, size_t sp, void* dst, size_t dp, int W, int H, int wx, int wy,   \
                           int op, int border, unsigned bval, int algo_h, int algo_v, void* stream) {     \
-        (void)algo_h; (void)algo_v;                                                                       \
         return run_morph(src, sp, 0, dst, dp, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, ELEM,           \
-                         (cudaStream_t)stream);                                                           \
+                         (cudaStream_t)stream, algo_h, algo_v);                                           \
     }                                                                                                     \
     int rmgpu_morph_batched_##SFX(const void* src, size_t sp, size_t simg, void* dst, size_t dp,          \
                                   size_t dimg, int batch, int W, int H, int wx, int wy, int op,           \
@@ -656,8 +889,7 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
     }                                                                                                     \
     int rmgpu_morph_host_##SFX(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int wx,  \
                                int wy, int op, int border, unsigned bval, int algo_h, int algo_v) {       \
-        (void)algo_h; (void)algo_v;                                                                       \
-        return host_morph(hsrc, sp, hdst, dp, W, H, wx, wy, op, border, bval, ELEM);                      \
+        return host_morph(hsrc, sp, hdst, dp, W, H, wx, wy, op, border, bval, ELEM, algo_h, algo_v);      \
     }
 
 MORPH_ENTRY(u8, 1)
@@ -760,13 +992,35 @@ int rmgpu_transpose_tiles_host(void* hdata, int elem, size_t n_tiles, int n, siz
     if (rs < (size_t)n) return fail(RMGPU_ERR_BAD_ARGUMENT, "bad tile stride");
     cudaStream_t s;
     if ((rc = host_stream(&s))) return rc;
-    const size_t span = ((n_tiles - 1) * step + (size_t)(n - 1) * rs + n) * elem;
+    // Only the tiles' own elements travel (transpose_tile touches nothing else, transpose.cpp:14-27,
+    // and concurrent calls on neighbouring tiles of one image must not lose each other's updates):
+    // contiguous tiles as one copy, tiles stacked at a uniform row pitch as one 2-D copy, anything
+    // else tile by tile. On the device the tiles are packed (row stride n, tile step n * n).
+    const size_t tb = (size_t)n * n * elem, rowb = (size_t)n * elem;
     DevBuf a;
     a.s = s;
-    RM_CUDA(scratch_alloc(&a.p, span, s));
-    RM_CUDA(cudaMemcpyAsync(a.p, hdata, span, cudaMemcpyHostToDevice, s));
-    if ((rc = tiles_impl(a.p, n_tiles, n, rs, step, elem, s))) return rc;
-    RM_CUDA(cudaMemcpyAsync(hdata, a.p, span, cudaMemcpyDeviceToHost, s));
+    RM_CUDA(scratch_alloc(&a.p, tb * n_tiles, s));
+    char* h = static_cast<char*>(hdata);
+    char* d = static_cast<char*>(a.p);
+    const bool packed = rs == (size_t)n && step == (size_t)n * n;
+    const bool stacked = step == (size_t)n * rs;
+    if (packed) {
+        RM_CUDA(cudaMemcpyAsync(d, h, tb * n_tiles, cudaMemcpyHostToDevice, s));
+    } else if (stacked) {
+        RM_CUDA(cudaMemcpy2DAsync(d, rowb, h, rs * elem, rowb, (size_t)n * n_tiles, cudaMemcpyHostToDevice, s));
+    } else {
+        for (size_t t = 0; t < n_tiles; ++t)
+            RM_CUDA(cudaMemcpy2DAsync(d + t * tb, rowb, h + t * step * elem, rs * elem, rowb, n, cudaMemcpyHostToDevice, s));
+    }
+    if ((rc = tiles_impl(a.p, n_tiles, n, n, (size_t)n * n, elem, s))) return rc;
+    if (packed) {
+        RM_CUDA(cudaMemcpyAsync(h, d, tb * n_tiles, cudaMemcpyDeviceToHost, s));
+    } else if (stacked) {
+        RM_CUDA(cudaMemcpy2DAsync(h, rs * elem, d, rowb, rowb, (size_t)n * n_tiles, cudaMemcpyDeviceToHost, s));
+    } else {
+        for (size_t t = 0; t < n_tiles; ++t)
+            RM_CUDA(cudaMemcpy2DAsync(h + t * step * elem, rs * elem, d + t * tb, rowb, rowb, n, cudaMemcpyDeviceToHost, s));
+    }
     RM_CUDA(cudaStreamSynchronize(s));
     return RMGPU_OK;
 }

@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 
 #include "rmgpu.h"
 
@@ -40,8 +42,18 @@ std::size_t padded_elems(int width) {
 
 int op_code(OpKind k) { return k == OpKind::Erode ? RMGPU_ERODE : RMGPU_DILATE; }
 
+// GPU planner hints for a config: a Calibrated config is honoured axis by axis, the paper's
+// thresholds (measured on ARM NEON) leave the choice to the planner (both give the same pixels)
+void hints(const StructuringElement& se, const DispatchConfig& cfg, int* ah, int* av) {
+    *ah = *av = RMGPU_ALGO_AUTO;
+    if (cfg.source != ThresholdSource::Calibrated) return;
+    *ah = rmgpu_resolve(RMGPU_ALGO_AUTO, se.width, RMGPU_AXIS_HORIZONTAL, cfg.threshold_h, cfg.threshold_v);
+    *av = rmgpu_resolve(RMGPU_ALGO_AUTO, se.height, RMGPU_AXIS_VERTICAL, cfg.threshold_h, cfg.threshold_v);
+}
+
 template <class T, class B>
-BasicImage<T> run(const BasicImage<T>& src, const StructuringElement& se, const B& border, int op) {
+BasicImage<T> run_algo(const BasicImage<T>& src, const StructuringElement& se, const B& border, int op, int ah,
+                       int av) {
     if (se.width < 1 || se.height < 1) throw Error(Errc::ZeroExtent, "structuring element extents must be >= 1");
     if (se.width % 2 == 0 || se.height % 2 == 0) throw Error(Errc::EvenExtent, "structuring element extents must be odd");
     BasicImage<T> dst(src.width(), src.height());
@@ -51,12 +63,20 @@ BasicImage<T> run(const BasicImage<T>& src, const StructuringElement& se, const 
     int rc;
     if constexpr (sizeof(T) == 1)
         rc = rmgpu_morph_host_u8(src.row(0), sp, dst.row(0), dp, src.width(), src.height(), se.width, se.height, op,
-                                 mode, border.value, RMGPU_ALGO_AUTO, RMGPU_ALGO_AUTO);
+                                 mode, border.value, ah, av);
     else
         rc = rmgpu_morph_host_u16(src.row(0), sp, dst.row(0), dp, src.width(), src.height(), se.width, se.height,
-                                  op, mode, border.value, RMGPU_ALGO_AUTO, RMGPU_ALGO_AUTO);
+                                  op, mode, border.value, ah, av);
     check(rc);
     return dst;
+}
+
+template <class T, class B>
+BasicImage<T> run(const BasicImage<T>& src, const StructuringElement& se, const B& border, int op,
+                  const DispatchConfig& cfg = {}) {
+    int ah, av;
+    hints(se, cfg, &ah, &av);
+    return run_algo(src, se, border, op, ah, av);
 }
 
 int border_mode(const BorderPolicy& b) {
@@ -137,10 +157,12 @@ Image vertical_pass_via_transpose(const Image& src, OpKind op, int window, const
 }
 
 Image morph_separable(const Image& src, OpKind op, const StructuringElement& se, const BorderPolicy& border,
-                      PassAlgorithm, PassAlgorithm, VerticalStrategy) {
+                      PassAlgorithm h, PassAlgorithm v, VerticalStrategy) {
     validate_window(se.width);  // separable.cpp:134-135
     validate_window(se.height);
-    return run(src, se, border, op_code(op));
+    // the explicit per-axis algorithms become GPU planner hints (rmgpu.h); both vertical strategies
+    // are the same fused column pass on the GPU
+    return run_algo(src, se, border, op_code(op), int(h), int(v));
 }
 Image morph_separable(const Image& src, OpKind op, const StructuringElement& se, const BorderPolicy& border,
                       PassAlgorithm h, PassAlgorithm v) {
@@ -154,17 +176,63 @@ PassAlgorithm resolve(PassAlgorithm algo, int window, Axis axis, const DispatchC
                                        cfg.threshold_h, cfg.threshold_v));
 }
 
-Image erode(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig&) { return run(s, se, b, RMGPU_ERODE); }
-Image dilate(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig&) { return run(s, se, b, RMGPU_DILATE); }
-Image opening(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig&) { return run(s, se, b, RMGPU_OPEN); }
-Image closing(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig&) { return run(s, se, b, RMGPU_CLOSE); }
-Image gradient(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig&) { return run(s, se, b, RMGPU_GRADIENT); }
+Image erode(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_ERODE, c); }
+Image dilate(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_DILATE, c); }
+Image opening(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_OPEN, c); }
+Image closing(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_CLOSE, c); }
+Image gradient(const Image& s, const StructuringElement& se, const BorderPolicy& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_GRADIENT, c); }
 
-Image16 erode(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig&) { return run(s, se, b, RMGPU_ERODE); }
-Image16 dilate(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig&) { return run(s, se, b, RMGPU_DILATE); }
-Image16 opening(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig&) { return run(s, se, b, RMGPU_OPEN); }
-Image16 closing(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig&) { return run(s, se, b, RMGPU_CLOSE); }
-Image16 gradient(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig&) { return run(s, se, b, RMGPU_GRADIENT); }
+Image16 erode(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_ERODE, c); }
+Image16 dilate(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_DILATE, c); }
+Image16 opening(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_OPEN, c); }
+Image16 closing(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_CLOSE, c); }
+Image16 gradient(const Image16& s, const StructuringElement& se, const BorderPolicy16& b, const DispatchConfig& c) { return run(s, se, b, RMGPU_GRADIENT, c); }
+
+// ---- dispatch config (dispatch.hpp:46-66) -------------------------------------------------------
+std::string format_config(const DispatchConfig& cfg) {
+    char buf[96];
+    const int n = rmgpu_format_config(cfg.threshold_h, cfg.threshold_v,
+                                      cfg.source == ThresholdSource::Calibrated ? RMGPU_SOURCE_CALIBRATED
+                                                                                : RMGPU_SOURCE_PAPER,
+                                      buf, sizeof buf);
+    return std::string(buf, std::min<std::size_t>(std::size_t(n), sizeof buf - 1));
+}
+
+DispatchConfig parse_config(const std::string& text) {
+    DispatchConfig cfg;
+    int src = RMGPU_SOURCE_PAPER;
+    check(rmgpu_parse_config(text.c_str(), &cfg.threshold_h, &cfg.threshold_v, &src));
+    cfg.source = src == RMGPU_SOURCE_CALIBRATED ? ThresholdSource::Calibrated : ThresholdSource::Paper;
+    return cfg;
+}
+
+DispatchConfig load_config(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw Error(Errc::IoError, "cannot open config '" + path + "'");
+    std::ostringstream text;
+    text << in.rdbuf();
+    try {
+        return parse_config(text.str());
+    } catch (const Error& e) {
+        throw Error(e.code(), path + ": " + e.what());
+    }
+}
+
+void save_config(const std::string& path, const DispatchConfig& cfg) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw Error(Errc::IoError, "cannot open '" + path + "' for writing");
+    out << format_config(cfg);
+    out.flush();
+    if (!out) throw Error(Errc::IoError, "failed writing config '" + path + "'");
+}
+
+DispatchConfig calibrate(int width, int height, const std::vector<int>& windows, int reps) {
+    DispatchConfig cfg;
+    check(rmgpu_calibrate(width, height, windows.data(), int(windows.size()), reps, &cfg.threshold_h,
+                          &cfg.threshold_v));
+    cfg.source = ThresholdSource::Calibrated;
+    return cfg;
+}
 
 // ---- transposes -------------------------------------------------------------------------------
 void transpose_tile(std::uint8_t* data, std::size_t stride, int n) { check(rmgpu_transpose_tiles_host(data, 1, 1, n, stride, 0)); }

@@ -24,6 +24,7 @@ struct MorphJob {
     int batch = 1;              // independent images (gridDim.z)
     size_t simg = 0, dimg = 0;  // bytes between consecutive images (batch > 1)
     cudaStream_t stream = nullptr;
+    int algo_h = 0, algo_v = 0;  // rmgpu_algo hints (Auto / Linear / VanHerk); never change results
 };
 
 // ---- launch bookkeeping (capi.cu): cached per (kernel, device) so a launch costs no extra

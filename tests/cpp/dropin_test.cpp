@@ -99,6 +99,23 @@ int main() {
     CHECK(equal_pixels(opening(o, make_se(5, 5), BorderPolicy16::replicate()), o));
     Image16 t16 = transpose_image(im16);
     CHECK(t16.width() == 30 && t16.at(3, 5) == im16.at(5, 3));
+    {  // morph_separable with every explicit algorithm / strategy (separable.hpp:44-55): same pixels
+        Image src(97, 61);
+        for (int y = 0; y < 61; ++y)
+            for (int x = 0; x < 97; ++x) src.at(x, y) = std::uint8_t((x * 37 + y * 101 + x * y) & 0xFF);
+        const StructuringElement se = make_se(21, 13);
+        const Image want = brute(src, OpKind::Dilate, se, BorderPolicy::constant(9));
+        for (auto h : {PassAlgorithm::Auto, PassAlgorithm::Linear, PassAlgorithm::VanHerk})
+            for (auto v : {PassAlgorithm::Auto, PassAlgorithm::Linear, PassAlgorithm::VanHerk})
+                for (auto st : {VerticalStrategy::Direct, VerticalStrategy::ViaTranspose})
+                    CHECK(equal_pixels(morph_separable(src, OpKind::Dilate, se, BorderPolicy::constant(9), h, v, st),
+                                       want));
+        DispatchConfig cal;
+        cal.threshold_h = 99;
+        cal.threshold_v = 3;
+        cal.source = ThresholdSource::Calibrated;
+        CHECK(equal_pixels(dilate(src, se, BorderPolicy::constant(9), cal), want));
+    }
     if (failures == 0) std::printf("ALL PASS\n");
     return failures == 0 ? 0 : 1;
 }

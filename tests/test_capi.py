@@ -101,7 +101,8 @@ def test_cpp_dropin_library_exports_reference_api():
                 "rectmorph::horizontal_pass(", "rectmorph::vertical_pass_direct(",
                 "rectmorph::vertical_pass_via_transpose(", "rectmorph::morph_separable(",
                 "rectmorph::linear_window_1d(", "rectmorph::van_herk_1d(", "rectmorph::resolve(",
-                "rectmorph::make_se("]:
+                "rectmorph::make_se(", "rectmorph::format_config", "rectmorph::parse_config(",
+                "rectmorph::load_config(", "rectmorph::save_config(", "rectmorph::calibrate("]:
         assert sym in out, sym
 
 
@@ -114,3 +115,64 @@ def test_no_cpu_fallback_in_product():
                 src += open(os.path.join(root, f)).read()
     assert "import oracle" not in src and "from oracle" not in src
     assert "liboracle" not in src and "librmref" not in src
+
+
+# ---- dispatch config + calibrate (dispatch.hpp:46-66): host-only, no device ------------------
+def test_config_text_round_trip_and_grammar():
+    cfg = pkg.DispatchConfig(33, 101, "calibrated")
+    text = pkg.format_config(cfg)
+    assert text == "threshold_h=33\nthreshold_v=101\nsource=calibrated\n"
+    assert pkg.parse_config(text) == cfg
+    assert pkg.format_config(pkg.DispatchConfig()) == "threshold_h=69\nthreshold_v=59\nsource=paper\n"
+    got = pkg.parse_config("# comment\n\nthreshold_h = 69\nthreshold_v=59\r\nsource= paper\n")
+    assert got == pkg.DispatchConfig(69, 59, "paper")
+    for bad in ["threshold_h=69\nthreshold_v=59\n",
+                "threshold_h=69\nthreshold_v=59\nsource=paper\nextra=1\n",
+                "threshold_h=68\nthreshold_v=59\nsource=paper\n",
+                "threshold_h=-3\nthreshold_v=59\nsource=paper\n",
+                "threshold_h=abc\nthreshold_v=59\nsource=paper\n",
+                "threshold_h=69\nthreshold_h=69\nthreshold_v=59\nsource=paper\n",
+                "threshold_h=69\nthreshold_v=59\nsource=guessed\n",
+                "threshold_h 69\nthreshold_v=59\nsource=paper\n"]:
+        with pytest.raises(pkg.Error) as e:
+            pkg.parse_config(bad)
+        assert e.value.code == pkg.Errc.BadConfig, bad
+    with pytest.raises(pkg.Error) as e:
+        pkg.parse_config("threshold_h=69\nthreshold_v=59\nsource=guessed\n")
+    assert "line 3" in str(e.value)
+
+
+def test_config_files(tmp_path):
+    cfg = pkg.DispatchConfig(45, 91, "calibrated")
+    path = str(tmp_path / "dispatch.txt")
+    pkg.save_config(path, cfg)
+    assert open(path).read() == "threshold_h=45\nthreshold_v=91\nsource=calibrated\n"
+    assert pkg.load_config(path) == cfg
+    with pytest.raises(pkg.Error) as e:
+        pkg.load_config(str(tmp_path / "missing.txt"))
+    assert e.value.code == pkg.Errc.IoError and "missing.txt" in str(e.value)
+
+
+def test_calibrate_validates_before_the_device():
+    for args, code in [((32, 32, [3, 5], 2), pkg.Errc.InsufficientReps),
+                       ((32, 32, [5, 3], 3), pkg.Errc.BadArgument),
+                       ((32, 32, [3, 4], 3), pkg.Errc.EvenExtent),
+                       ((32, 32, [], 3), pkg.Errc.BadArgument),
+                       ((0, 32, [3], 3), pkg.Errc.BadArgument)]:
+        with pytest.raises(pkg.Error) as e:
+            pkg.calibrate(*args)
+        assert e.value.code == code, args
+
+
+def test_cpp_config_binary(tmp_path):
+    # the reference's config API, compiled against the drop-in header and run without a GPU
+    src = os.path.join(ROOT, "tests", "cpp", "config_test.cpp")
+    exe = str(tmp_path / "config_test")
+    pkgdir = os.path.join(ROOT, "paper_2002_09474_b200")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", exe,
+                        "-L", pkgdir, "-lrectmorph_b200", "-lrmgpu", f"-Wl,-rpath,{pkgdir}"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "config_test ok" in r.stdout

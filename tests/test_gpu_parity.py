@@ -518,60 +518,81 @@ def test_cfg1_full_size(gpu, reference, restatement):
 
 
 def test_cfg3_transposes_full_size(gpu, restatement):
+    # BASELINE cfg3 at full size: 8192^2 u8 and u16 images and all 2^24 8x8 / 16x16 u8 tiles,
+    # every element compared with the closed form (x^T; per tile t[i][j] <- t[j][i],
+    # transpose.hpp:19-30), the inputs pinned to the generator the restatement shares
     import torch
     for dtype, seed in ((np.uint8, 3), (np.uint16, 30)):
         src = torch.empty((8192, 8192), dtype=torch.uint8 if dtype == np.uint8 else torch.uint16, device="cuda")
         gpu.generate_device(src, seed)
         dst = torch.empty_like(src)
         gpu.transpose_device(src, dst)
-        back = torch.empty_like(src)
-        gpu.transpose_device(dst, back)
         torch.cuda.synchronize()
-        # involution + spot rows against the generator (oracle) -- size-independent properties
-        assert torch.equal(back.view(torch.uint8), src.view(torch.uint8))
-        host_rows = restatement.generate(8192, 4, seed, dtype=dtype)
-        assert np.array_equal(to_host(dst[:, :4]).T, host_rows)
-    # 2^24 tiles would be 1-4 GiB: check a 2^20 slice exactly against the restatement
-    for n in (8, 16):
-        t = torch.empty((1 << 20) * n * n // 4096, 4096, dtype=torch.uint8, device="cuda")
-        gpu.generate_device(t, 31 if n == 8 else 32)
-        host = to_host(t).ravel().copy()
+        s8 = src.view(torch.uint8).view(8192, 8192, -1)  # compare as bytes (uint16 eq needs no arithmetic)
+        assert torch.equal(dst.view(torch.uint8).view(8192, 8192, -1), s8.transpose(0, 1).contiguous()), dtype
+        assert np.array_equal(to_host(src[:4]), restatement.generate(8192, 4, seed, dtype=dtype))
+    for n, seed in ((8, 31), (16, 32)):
+        t = torch.empty(((1 << 24) * n * n // 4096, 4096), dtype=torch.uint8, device="cuda")
+        gpu.generate_device(t, seed)
+        want = t.view(-1, n, n).transpose(1, 2).contiguous()
+        assert np.array_equal(to_host(t[:2]), restatement.generate(4096, 2, seed))
         gpu.transpose_tiles_device(t, n)
         torch.cuda.synchronize()
-        assert np.array_equal(to_host(t).ravel(), restatement.transpose_tiles(host, n))
+        assert torch.equal(t.view(-1, n, n), want), n
+        del t, want
+        torch.cuda.empty_cache()
 
 
-def test_cfg4_opening_u16_batch(gpu, restatement):
+def test_cfg4_opening_u16_full_batch(gpu, restatement):
+    # BASELINE cfg4 at full size: all 512 u16 1024^2 images (seed 4, stream = image index), one
+    # batched opening 21x21, every image compared with the restatement (host threads in parallel;
+    # van Herk in the restatement for speed -- its algorithms are pinned equal in test_oracle)
+    import concurrent.futures as cf
     import torch
-    B = 8  # subset of the 512-image batch: every image is independent
-    imgs = torch.empty((B, 1024, 1024), dtype=torch.uint16, device="cuda")
+    from oracle import VANHERK
+    B, N = 512, 1024
+    imgs = torch.empty((B, N, N), dtype=torch.uint16, device="cuda")
     for b in range(B):
         gpu.generate_device(imgs[b], 4, stream_id=b)
     out = torch.empty_like(imgs)
     gpu.morph_batched_device(imgs, out, 21, 21, OPEN)
     torch.cuda.synchronize()
     host = to_host(out)
-    for b in (0, B - 1):
-        src = restatement.generate(1024, 1024, 4, stream=b, dtype=np.uint16)
-        assert np.array_equal(host[b], restatement.morph(src, 21, 21, OPEN))
+    assert host.shape == (B, N, N)
+
+    def check(b):
+        src = restatement.generate(N, N, 4, stream=b, dtype=np.uint16)
+        return b, np.array_equal(host[b], restatement.morph(src, 21, 21, OPEN, h_algo=VANHERK, v_algo=VANHERK))
+
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 8) as ex:
+        bad = [b for b, ok in ex.map(check, range(B)) if not ok]
+    assert not bad, bad
 
 
-def test_cfg5_bands_crop_exact(gpu, restatement, reference):
-    # cfg5 (32768^2 u8, dilate 63x63) is checked on 4 row bands of the full-width image: each band
-    # result equals the reference on band+halo (exact by the band argument, tested above)
+def test_cfg5_full_image_as_row_bands(gpu, reference):
+    # BASELINE cfg5 at full size: the 32768^2 u8 image dilated 63x63, computed as 8 virtual row
+    # bands (the multi-GPU split on one GPU: each band sees only its rows plus 31-row halos,
+    # rmgpu_morph_band_u8), bit-exact against the reference on all host threads
     import torch
-    W, H, g = 32768, 1024, 31
+    W = H = 32768
+    g, nb = 31, 8
     img = torch.empty((H, W), dtype=torch.uint8, device="cuda")
     gpu.generate_device(img, 5)
     out = torch.empty_like(img)
-    gpu.morph_device(img, out, 63, 63, DILATE)
+    rows = H // nb
+    for k in range(nb):
+        r0, r1 = k * rows, (k + 1) * rows
+        a, z = max(0, r0 - g), min(H, r1 + g)
+        band = img[a:z].clone()  # a separate buffer, as a rank would hold it
+        gpu.morph_band_device(band, r0 - a, z - r1, out[r0:r1], 63, 63, DILATE)
+        del band
     torch.cuda.synchronize()
-    host = to_host(img)
     got = to_host(out)
-    for r0 in (0, 300, H - 64):
-        a, z = max(0, r0 - g), min(H, r0 + 64 + g)
-        want = reference.morph(host[a:z], 63, 63, DILATE, nthreads=8)[r0 - a:r0 - a + 64]
-        assert np.array_equal(got[r0:r0 + 64], want)
+    host = to_host(img)
+    del img, out
+    torch.cuda.empty_cache()
+    want = reference.morph(host, 63, 63, DILATE, nthreads=os.cpu_count() or 8)
+    assert np.array_equal(got, want)
 
 
 def test_cpp_dropin_binary(gpu, tmp_path):
@@ -585,3 +606,75 @@ def test_cpp_dropin_binary(gpu, tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ALL PASS" in r.stdout
+
+
+def test_morph_separable_api(gpu, reference, restatement):
+    # morph_separable (separable.hpp:44-55, separable.cpp:130-157) with every explicit algorithm /
+    # strategy combination -- results never depend on them -- against the reference's own function
+    from oracle import LINEAR, VANHERK
+    rng = np.random.default_rng(44)
+    for c in range(12):
+        w, h = int(rng.integers(1, 300)), int(rng.integers(1, 200))
+        wx, wy = 2 * int(rng.integers(0, 30)) + 1, 2 * int(rng.integers(0, 30)) + 1
+        op = int(rng.integers(0, 2))
+        border, bval = int(rng.integers(0, 2)), int(rng.integers(0, 256))
+        img = restatement.generate(w, h, 500 + c)
+        for ha, va, vs in ((1, 1, 0), (2, 2, 1), (1, 2, 1), (2, 1, 0), (0, 0, 0)):
+            want = reference.morph_separable(img, wx, wy, op, border, bval, ha, va, vs)
+            got = gpu.morph_separable(img, gpu.OpKind(op), gpu.StructuringElement(wx, wy),
+                                      gpu.BorderPolicy(border, bval), gpu.PassAlgorithm(ha), gpu.PassAlgorithm(va),
+                                      gpu.VerticalStrategy(vs))
+            assert np.array_equal(got, want), (c, w, h, wx, wy, op, ha, va, vs)
+    assert LINEAR == 1 and VANHERK == 2
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_algorithm_hints_never_change_results(gpu, restatement, dtype):
+    # the C-ABI's algo_h / algo_v hints (rmgpu.h): Linear on a long wing runs that axis as the
+    # direct sliding window, VanHerk / Auto the planner's kernels -- every combination exact
+    import torch
+    rng = np.random.default_rng(45 + np.dtype(dtype).itemsize)
+    mx = int(np.iinfo(dtype).max)
+    es = np.dtype(dtype).itemsize
+    L = gpu.lib()
+    fn = L.rmgpu_morph_u8 if es == 1 else L.rmgpu_morph_u16
+    for c in range(24):
+        w, h = int(rng.integers(1, 400)), int(rng.integers(1, 300))
+        wx, wy = 2 * int(rng.integers(0, 40)) + 1, 2 * int(rng.integers(0, 40)) + 1
+        op = int(rng.integers(0, 5))
+        border, bval = int(rng.integers(0, 2)), int(rng.integers(0, mx + 1))
+        img = restatement.generate(w, h, 900 + c, dtype=dtype)
+        want = restatement.morph(img, wx, wy, op, border, bval)
+        pad = (-w) % (16 // es)
+        for ah, av in ((1, 1), (1, 2), (2, 1), (2, 2), (1, 0), (0, 1)):
+            src = to_device(img, pad)
+            dst = empty_device(img.shape, dtype, pad)
+            rc = fn(src.data_ptr(), src.stride(0) * es, dst.data_ptr(), dst.stride(0) * es, w, h, wx, wy, op, border,
+                    bval, ah, av, None)
+            assert rc == 0, L.rmgpu_last_error()
+            torch.cuda.synchronize()
+            assert np.array_equal(to_host(dst), want), (c, w, h, wx, wy, op, border, ah, av)
+
+
+def test_calibrate_on_gpu(gpu, tmp_path):
+    # calibrate (dispatch.cpp:180-248) on the B200: thresholds from the swept set, marked
+    # calibrated; a calibrated config steers the planner and still gives the same pixels
+    cfg = gpu.calibrate(512, 384, [3, 5, 7, 9, 15, 31], 3)
+    assert cfg.source == "calibrated"
+    assert cfg.threshold_h in (1, 3, 5, 7, 9, 15, 31) and cfg.threshold_v in (1, 3, 5, 7, 9, 15, 31)
+    img = np.random.default_rng(9).integers(0, 256, (301, 277), dtype=np.uint8)
+    for t in (cfg, gpu.DispatchConfig(101, 101, "calibrated"), gpu.DispatchConfig(1, 1, "calibrated")):
+        for (wx, wy) in ((31, 15), (9, 63), (3, 3)):
+            a = gpu.erode(img, gpu.make_se(wx, wy), gpu.BorderPolicy(), t)
+            b = gpu.erode(img, gpu.make_se(wx, wy))
+            assert np.array_equal(a, b), (t, wx, wy)
+    src = os.path.join(ROOT, "tests", "cpp", "config_test.cpp")
+    exe = str(tmp_path / "config_test")
+    pkgdir = os.path.join(ROOT, "paper_2002_09474_b200")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", exe,
+                        "-L", pkgdir, "-lrectmorph_b200", "-lrmgpu", f"-Wl,-rpath,{pkgdir}"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe, str(tmp_path), "--gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "config_test ok" in r.stdout
