@@ -678,3 +678,29 @@ def test_calibrate_on_gpu(gpu, tmp_path):
     r = subprocess.run([exe, str(tmp_path), "--gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "config_test ok" in r.stdout
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_row_bands_with_overlapped_exchange_one_gpu(gpu, restatement, dtype):
+    # the multi-GPU row-band pipeline driven from one process (shard.morph_bands_local): band
+    # buffers holding only their own rows, halos copied between them on each band's stream while
+    # the interior rows are computed, then the edge rows -- rmgpu_morph_band_* behind a real
+    # exchange, against the whole-image oracle
+    import torch
+    from paper_2002_09474_b200.shard import morph_bands_local
+    rng = np.random.default_rng(61 + np.dtype(dtype).itemsize)
+    mx = int(np.iinfo(dtype).max)
+    for c in range(10):
+        w, h = int(rng.integers(16, 900)), int(rng.integers(64, 700))
+        gy = int(rng.integers(1, 40))
+        nb = int(rng.integers(2, max(3, min(8, h // max(gy, 1)))))
+        wx, wy = 2 * int(rng.integers(0, 30)) + 1, 2 * gy + 1
+        op = int(rng.integers(0, 2)) if c % 3 else GRADIENT
+        border, bval = int(rng.integers(0, 2)), int(rng.integers(0, mx + 1))
+        img = restatement.generate(w, h, 1300 + c, dtype=dtype)
+        src = to_device(img)
+        out = empty_device(img.shape, dtype)
+        morph_bands_local(src, out, nb, wx, wy, op, border, bval)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(out), restatement.morph(img, wx, wy, op, border, bval)), \
+            (c, w, h, wx, wy, op, border, nb)

@@ -11,7 +11,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2002_09474_b200.shard import band_plan, batch_shard, exchange_halos, neighbours
+from paper_2002_09474_b200.shard import (_band_pieces, band_plan, batch_shard, exchange_halos, interior_rows,
+                                          neighbours, start_halo_exchange)
 
 
 def test_batch_shard_covers_everything():
@@ -60,12 +61,26 @@ def _worker(rank, world, port, h, w, wx, wy, op, border, bval, q):
         # local buffer: band rows from "our memory", halo rows poisoned until the exchange
         buf = torch.full((band.buffer_rows, w), 0xEE, dtype=torch.uint8)
         buf[band.above:band.above + band.rows] = torch.from_numpy(full[band.y0:band.y0 + band.rows])
-        exchange_halos(buf, band, world, rank, wing, dist=dist)
+        # the overlapped schedule of morph_band_overlapped: issue the exchange (received straight
+        # into the poisoned halo rows), compute the interior pieces while it is in flight, wait,
+        # compute the edge pieces. The oracle on the piece's rows stands in for rmgpu_morph_band_u8
+        # (same semantics: the piece's first / last context rows are its border); an interior piece
+        # that read a halo row would see poison or a racing receive and differ.
+        out = torch.zeros((band.rows, w), dtype=torch.uint8)
+
+        def launch(src, above, below, dst):
+            n = dst.shape[0]
+            local = R.morph(np.ascontiguousarray(src[:above + n + below].numpy()), wx, wy, op, border, bval)
+            dst.copy_(torch.from_numpy(np.ascontiguousarray(local[above:above + n])))
+
+        reqs = start_halo_exchange(buf, band, world, rank, wing, dist=dist)
+        _band_pieces(buf, out, band, wing, launch, bool(reqs), "interior")
+        for req in reqs:
+            req.wait()
+        _band_pieces(buf, out, band, wing, launch, bool(reqs), "edges")
         want_buf = full[band.in_y0:band.in_y0 + band.buffer_rows]
         ok_exchange = bool(np.array_equal(buf.numpy(), want_buf))
-        # the band compute (oracle stands in for rmgpu_morph_band_u8): crop of the buffer result
-        local = R.morph(np.ascontiguousarray(buf.numpy()), wx, wy, op, border, bval)
-        mine = torch.from_numpy(np.ascontiguousarray(local[band.above:band.above + band.rows]))
+        mine = out
         sizes = [band_plan(h, world, r, wing).rows for r in range(world)]
         parts = [torch.empty((s, w), dtype=torch.uint8) for s in sizes]
         dist.all_gather(parts, mine) if len(set(sizes)) == 1 else _gather_ragged(parts, mine, rank, world)
@@ -86,7 +101,7 @@ def _gather_ragged(parts, mine, rank, world):
 
 
 @pytest.mark.parametrize("h,wx,wy,op,border,bval", [(64, 3, 3, 0, 0, 0), (101, 5, 31, 1, 0, 0), (77, 7, 21, 0, 1, 9),
-                                                     (62, 1, 61, 1, 0, 0)])
+                                                     (62, 1, 61, 1, 0, 0), (200, 9, 15, 4, 0, 0), (90, 3, 29, 4, 1, 77)])
 def test_row_bands_gloo_world2(h, wx, wy, op, border, bval):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -100,3 +115,37 @@ def test_row_bands_gloo_world2(h, wx, wy, op, border, bval):
         assert p.exitcode == 0
     assert all(r[0] for r in res), "halo exchange delivered wrong rows"
     assert all(r[1] for r in res), "banded result differs from the whole-image oracle"
+
+
+def test_band_pieces_cover_the_band_single_process():
+    # the interior / edge decomposition of morph_band_overlapped, every band of several splits:
+    # the interior pieces never read a halo row (poisoned until "arrival"), edges + interior
+    # reproduce the whole-image result exactly
+    import oracle
+    R = oracle.restatement()
+    for h, w, wy, nb in ((97, 33, 11, 3), (64, 20, 31, 2), (300, 17, 21, 5), (40, 9, 3, 8)):
+        full = R.generate(w, h, h + wy)
+        want = R.morph(full, 5, wy, 1)
+        wing = wy // 2
+        got = np.zeros_like(full)
+        for k in range(nb):
+            band = band_plan(h, nb, k, wing)
+            if band.rows == 0:
+                continue
+            buf = torch.full((band.buffer_rows, w), 0xEE, dtype=torch.uint8)
+            buf[band.above:band.above + band.rows] = torch.from_numpy(full[band.y0:band.y0 + band.rows])
+            out = torch.zeros((band.rows, w), dtype=torch.uint8)
+
+            def launch(src, above, below, dst):
+                n = dst.shape[0]
+                local = R.morph(np.ascontiguousarray(src[:above + n + below].numpy()), 5, wy, 1)
+                dst.copy_(torch.from_numpy(np.ascontiguousarray(local[above:above + n])))
+
+            pending = band.above > 0 or band.below > 0
+            _band_pieces(buf, out, band, wing, launch, pending, "interior")
+            lo, hi = interior_rows(band, wing)
+            if pending:  # halos arrive
+                buf[:] = torch.from_numpy(full[band.in_y0:band.in_y0 + band.buffer_rows])
+            _band_pieces(buf, out, band, wing, launch, pending, "edges")
+            got[band.y0:band.y0 + band.rows] = out.numpy()
+        assert np.array_equal(got, want), (h, w, wy, nb)
