@@ -58,7 +58,26 @@ def parse_args(argv=None):
     p.add_argument("--streams", type=int, default=2,
                    help="streams the step graph forks its independent operations over (1 = serial)")
     p.add_argument("--soak-seconds", type=float, default=1.5)
+    p.add_argument("--no-self-check", action="store_true",
+                   help="skip the bit-exact check of the timed outputs against the CPU reference")
+    p.add_argument("--dry-run", action="store_true",
+                   help="CPU only (gloo): exercise the N-rank launch, barriers and max-over-ranks timing "
+                        "with the oracle as the step; no GPU, no kernel")
     return p.parse_args(argv)
+
+
+def maybe_spawn(args, argv) -> int | None:
+    """`bench.py --gpus N` outside torchrun starts N ranks itself (torch.distributed.run, one
+    process per GPU, rendezvous on 127.0.0.1) and returns their exit code; None = already a rank."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
 
 
 def peaks():
@@ -76,8 +95,10 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = None
 
     def init(self, backend="nccl"):
+        self.backend = backend
         if self.world > 1:
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -92,7 +113,8 @@ class Dist:
         if self.pg is None:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+        on_gpu = self.backend == "nccl" and torch.cuda.is_available()
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
@@ -179,6 +201,7 @@ class Cfg2:
         self.inputs = [base.clone() for _ in range(self.NB)]
         self.outputs = [torch.empty_like(base) for _ in range(self.NB)]
         self.cursor = 0
+        self.written = {}
         n = self.size * self.size
         self.ops = []
         for (wx, wy, op) in self.ops_list:
@@ -188,7 +211,29 @@ class Cfg2:
         wx, wy, op = spec
         i = self.cursor % self.NB
         self.cursor += 1
+        self.written[i] = spec
         self.pkg.morph_device(self.inputs[i], self.outputs[i], wx, wy, op)
+
+    def self_check(self) -> dict:
+        """Every output buffer of the timed step graphs against the reference (all host threads):
+        bit-exact or the run is reported as failed."""
+        import torch
+        R, port, nthreads = _reference_checker(self)
+        if R is None:
+            import oracle
+            R, nthreads = oracle.restatement(), 1
+        want = {}
+        bad = []
+        torch.cuda.synchronize()
+        for i, spec in sorted(self.written.items()):
+            if spec not in want:
+                wx, wy, op = spec
+                want[spec] = (R.morph(self.img, wx, wy, op, nthreads=nthreads) if nthreads > 1
+                              else R.morph(self.img, wx, wy, op))
+            if not np.array_equal(self.outputs[i].cpu().numpy(), want[spec]):
+                bad.append({"buffer": i, "op": list(spec)})
+        return {"checked_outputs": len(self.written), "distinct_ops": len(want), "bit_exact": not bad,
+                "mismatches": bad[:8], "against": "reference (oracle/_ref)" if nthreads > 1 else "restatement"}
 
     def config(self):
         return {"workload": "cfg2: 4096x4096 u8, erode+dilate per window, windows "
@@ -222,9 +267,9 @@ class Cfg2:
         return len(self.ops_list) * self.size * self.size
 
     # CPU legs (reference code, oracle/_ref): one full step = the same 16 operations
-    def ref_step(self, R, nthreads, out):
+    def ref_step(self, R, nthreads, out, th=69, tv=59):
         for (wx, wy, op) in self.ops_list:
-            R.morph(self.img, wx, wy, op, nthreads=nthreads, out=out)
+            R.morph(self.img, wx, wy, op, threshold_h=th, threshold_v=tv, nthreads=nthreads, out=out)
         return self.out_pixels_per_step()
 
 
@@ -245,6 +290,7 @@ class Cfg1(Cfg2):
         self.inputs = [base.clone() for _ in range(self.NB)]
         self.outputs = [torch.empty_like(base) for _ in range(self.NB)]
         self.cursor = 0
+        self.written = {}
         n = self.img.size
         self.ops = [(f"{'erode' if op == ERODE else 'dilate'} 3x3", (wx, wy, op), 2 * n, n)
                     for (wx, wy, op) in self.ops_list]
@@ -323,9 +369,24 @@ class Cfg4:
         nbytes = self.h_in.numel() * 2
         return nbytes, nbytes
 
+    def self_check(self) -> dict:
+        """Three images of the timed batch (first, middle, last) against the restatement."""
+        import oracle
+        from oracle import VANHERK
+        R = oracle.restatement()
+        bad = []
+        picks = sorted({0, self.count // 2, self.count - 1}) if self.count else []
+        for k in picks:
+            src = R.generate(self.SIZE, self.SIZE, 4, self.first + k, np.uint16)
+            got = self.dst[k].contiguous().view(torch_u8()).cpu().numpy().view(np.uint16)
+            if not np.array_equal(got, R.morph(src, self.WIN, self.WIN, OPEN, h_algo=VANHERK, v_algo=VANHERK)):
+                bad.append(self.first + k)
+        return {"checked_images": [self.first + k for k in picks], "bit_exact": not bad, "mismatches": bad,
+                "against": "restatement (u16: no reference)"}
+
     ref_port = True  # u16: the reference is u8-only; the CPU leg is the oracle restatement (SURVEY.md 8c)
 
-    def ref_step(self, R, nthreads, out):
+    def ref_step(self, R, nthreads, out, th=69, tv=59):
         R.morph(self.img, self.WIN, self.WIN, OPEN)
         return self.SIZE * self.SIZE
 
@@ -361,10 +422,31 @@ class Cfg5:
                      npx)]
 
     def launch(self, spec):
-        from paper_2002_09474_b200.shard import exchange_halos, morph_band
-        if self.dist.world > 1:
-            exchange_halos(self.buf, self.band, self.dist.world, self.dist.rank, self.WIN // 2, dist=self.dist.pg)
-        morph_band(self.buf, self.out, self.band, self.WIN, self.WIN, DILATE)
+        from paper_2002_09474_b200.shard import morph_band, morph_band_overlapped
+        if self.dist.world > 1:  # interior rows computed while the halos fly, edge rows after
+            morph_band_overlapped(self.buf, self.out, self.band, self.dist.world, self.dist.rank, self.WIN,
+                                  self.WIN, DILATE, dist=self.dist.pg)
+        else:
+            morph_band(self.buf, self.out, self.band, self.WIN, self.WIN, DILATE)
+
+    def self_check(self) -> dict:
+        """Two 512-row crops of the band (first and last rows) against the reference on the same
+        input rows plus their halo (exact: a band's rows see only the rows they would see whole)."""
+        R, port, nthreads = _reference_checker(self)
+        if R is None:
+            return {"bit_exact": None, "note": "reference not built"}
+        b, g = self.band, self.WIN // 2
+        bad, crops = [], []
+        for r0 in sorted({0, max(0, b.rows - 512)}):
+            r1 = min(b.rows, r0 + 512)
+            a = max(0, b.above + r0 - g)
+            z = min(b.buffer_rows, b.above + r1 + g)
+            host = self.buf[a:z].cpu().numpy()
+            want = R.morph(host, self.WIN, self.WIN, DILATE, nthreads=nthreads)[b.above + r0 - a:b.above + r1 - a]
+            crops.append([b.y0 + r0, b.y0 + r1])
+            if not np.array_equal(self.out[r0:r1].cpu().numpy(), want):
+                bad.append([b.y0 + r0, b.y0 + r1])
+        return {"checked_rows": crops, "bit_exact": not bad, "mismatches": bad, "against": "reference (oracle/_ref)"}
 
     def config(self):
         return {"workload": f"cfg5: {self.SIZE}x{self.SIZE} u8 dilate {self.WIN}x{self.WIN} (seed 5), row bands",
@@ -389,8 +471,8 @@ class Cfg5:
         torch.cuda.synchronize()
         return self.h_in.numel(), self.h_out.numel()
 
-    def ref_step(self, R, nthreads, out):
-        R.morph(self.img, self.WIN, self.WIN, DILATE, nthreads=nthreads, out=out)
+    def ref_step(self, R, nthreads, out, th=69, tv=59):
+        R.morph(self.img, self.WIN, self.WIN, DILATE, threshold_h=th, threshold_v=tv, nthreads=nthreads, out=out)
         return self.img.size
 
 
@@ -437,6 +519,23 @@ class Cfg3:
         else:
             self.pkg.transpose_tiles_device(self.tiles16, 16)
 
+    def self_check(self) -> dict:
+        """Image transposes: every element against x^T. Tiles: transposed an even number of times
+        by the timed steps (in place), so they must equal their generator input again; plus one
+        extra call checked per element against the closed form."""
+        import torch
+        ok = bool(torch.equal(self.t8, self.a8.t().contiguous()))
+        ok &= bool(torch.equal(self.t16.view(torch.uint8).view(8192, 8192, 2),
+                               self.a16.view(torch.uint8).view(8192, 8192, 2).transpose(0, 1).contiguous()))
+        for t, n in ((self.tiles8, 8), (self.tiles16, 16)):
+            before = t.view(-1, n, n)[:1 << 16].transpose(1, 2).contiguous()
+            self.pkg.transpose_tiles_device(t, n)
+            torch.cuda.synchronize()
+            ok &= bool(torch.equal(t.view(-1, n, n)[:1 << 16], before))
+            self.pkg.transpose_tiles_device(t, n)  # back
+        return {"bit_exact": ok, "checked": "both 8192^2 images (all elements); 2^16 tiles of each size",
+                "against": "closed form (x^T)"}
+
     def config(self):
         return {"workload": "cfg3: transpose 8192^2 u8 + 8192^2 u16, 2^24 8x8 + 2^24 16x16 u8 tiles in place",
                 "unit_note": "value counts transposed elements (Gelem/s)", "l2": "no flush: buffers >> L2",
@@ -462,82 +561,150 @@ class Cfg3:
     def e2e_pixels_per_step(self):
         return self.a8.numel()  # the e2e leg moves and transposes the 8192^2 u8 image
 
-    def ref_step(self, R, nthreads, out):
+    def ref_step(self, R, nthreads, out, th=69, tv=59):
         R.transpose_image(self.img, nthreads=nthreads)
         return self.img.size
+
+
+def torch_u8():
+    import torch
+    return torch.uint8
 
 
 WORKLOADS = {"cfg1": Cfg1, "cfg2": Cfg2, "cfg3": Cfg3, "cfg4": Cfg4, "cfg5": Cfg5}
 
 
 # ---------------------------------------------------------------------------------------------
+def _reference_checker(wl):
+    """(checker, is_port, threads): the reference's own code (oracle/_ref) on every host thread,
+    pinned one per CPU; for u16 (no reference) the restatement on one thread."""
+    import oracle
+    port = getattr(wl, "ref_port", False)
+    if not port and not oracle.Reference.available():
+        return None, port, 0
+    if port:
+        return oracle.restatement(), True, 1
+    R = oracle.reference()
+    R.set_pinning(True)
+    return R, False, (os.cpu_count() or 1)
+
+
+def _median_step(wl, R, nthreads, out, reps, **kw) -> tuple[float, int]:
+    """timing::median_ns (timing.hpp:22-53): one warm-up, the median of `reps` timed steps."""
+    wl.ref_step(R, nthreads, out, **kw)
+    times, px = [], 0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        px = wl.ref_step(R, nthreads, out, **kw)
+        times.append(time.perf_counter() - t0)
+    return statistics.median(times), px
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference_arm(args, dist: Dist):
     """--impl reference: the reference's own CPU implementation (oracle/_ref, compiled from the
     reference sources) on the host cores, same workload/metric. Rank 0 only."""
     if dist.rank != 0:
         return 0
-    import oracle
     wl = WORKLOADS[args.workload](dist)
-    port = getattr(wl, "ref_port", False)
-    if not port and not oracle.Reference.available():
+    R, port, nthreads = _reference_checker(wl)
+    if R is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/librmref.so not built"}))
         return 0
-    R = oracle.restatement() if port else oracle.reference()
-    nthreads = 1 if port else (os.cpu_count() or 1)
     out = np.empty_like(wl.img)
-    for _ in range(args.warmup):
+    for _ in range(max(0, args.warmup - 1)):
         wl.ref_step(R, nthreads, out)
-    t0 = time.perf_counter()
-    px = 0
-    for _ in range(args.steps):
-        px += wl.ref_step(R, nthreads, out)
-    dt = time.perf_counter() - t0
-    value = px / dt / 1e9
+    med, px = _median_step(wl, R, nthreads, out, max(1, args.steps))
+    value = px / med / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": med * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype,
             "data": "synthetic (seeded generator, SURVEY.md 8d)", "config": wl.config(),
             "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": nthreads,
-                             "kind": "port" if port else "reference",
+                             "kind": "port" if port else "reference", "cpu_model": _cpu_model(),
+                             "timing": "median of the timed steps after one warm-up (timing.hpp:22-53)",
                              "sample": (f"one {wl.name} image per step through the oracle restatement (u16 has no "
                                         "reference implementation), 1 thread") if port else
                                        (f"{wl.name} sample per step; reference rectmorph (oracle/_ref, -O3, "
-                                        f"DispatchConfig paper 69/59) on {nthreads} threads via row bands")},
+                                        f"DispatchConfig paper 69/59) on {nthreads} pinned threads via row bands")},
             "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
 def cpu_baseline(wl) -> dict | None:
-    port = getattr(wl, "ref_port", False)
+    """The reference on the host cores beside our numbers (reported, not a target): all threads
+    (median of 5 steps), one thread (median of 3), and all threads with the thresholds the
+    reference's own calibrate() picks on this host (dispatch.cpp:180-248)."""
     try:
-        import oracle
-        if not port and not oracle.Reference.available():
-            return None
-        R = oracle.restatement() if port else oracle.reference()
+        R, port, nthreads = _reference_checker(wl)
     except Exception:
         return None
-    nthreads = 1 if port else (os.cpu_count() or 1)
+    if R is None:
+        return None
     out = np.empty_like(wl.img)
-    wl.ref_step(R, nthreads, out)  # warm
+    med, px = _median_step(wl, R, nthreads, out, 5)
+    res = {"value": px / med / 1e9, "unit": "Gpixel/s", "cores": nthreads, "kind": "port" if port else "reference",
+           "cpu_model": _cpu_model(), "timing": "median of 5 steps after one warm-up (timing.hpp:22-53)",
+           "sample": f"{wl.name} CPU sample ({px} output px per step) through "
+                     + ("the oracle restatement (u16: no reference), 1 thread" if port else
+                        f"the reference rectmorph (oracle/_ref, DispatchConfig paper 69/59) on {nthreads} pinned "
+                        "host threads (row bands + halo)")}
+    if not port:
+        med1, _ = _median_step(wl, R, 1, out, 3)
+        res["single_thread"] = {"ms_per_step": med1 * 1e3, "value": px / med1 / 1e9}
+        if wl.name != "cfg3":
+            th, tv = R.calibrate(1024, 1024, list(range(3, 128, 8)), 3)
+            medc, _ = _median_step(wl, R, nthreads, out, 5, th=th, tv=tv)
+            res["calibrated"] = {"threshold_h": th, "threshold_v": tv, "value": px / medc / 1e9,
+                                 "ms_per_step": medc * 1e3,
+                                 "how": "reference calibrate(1024, 1024, windows 3..127 step 8, reps 3) on this host"}
+    return res
+
+
+def run_dry(args, dist: Dist) -> int:
+    """--dry-run: the multi-rank plumbing on CPU (gloo): every rank runs a small oracle morphology as
+    its step between barriers, the time is the max over ranks, rank 0 prints the contract line."""
+    import oracle
+    dist.init("gloo")
+    R = oracle.restatement()
+    img = R.generate(512, 512, 100 + dist.rank)
+    for _ in range(args.warmup):
+        R.morph(img, 15, 15, ERODE)
+    dist.barrier()
     t0 = time.perf_counter()
-    reps = 0
-    px = 0
-    while True:
-        px += wl.ref_step(R, nthreads, out)
-        reps += 1
-        if time.perf_counter() - t0 > 3.0 or reps >= 5:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": nthreads, "kind": "port" if port else "reference",
-            "sample": f"{reps} x {wl.name} CPU sample ({px // max(reps, 1)} output px each) through "
-                      + ("the oracle restatement (u16: no reference), 1 thread" if port else
-                         f"the reference rectmorph (oracle/_ref) on {nthreads} host threads (row bands + halo)")}
+    for _ in range(args.steps):
+        R.morph(img, 15, 15, ERODE)
+    dist.barrier()
+    dt = dist.max(time.perf_counter() - t0)
+    if dist.rank == 0:
+        print(json.dumps({"metric": METRIC, "value": dist.world * img.size * args.steps / dt / 1e9,
+                          "unit": "Gpixel/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "u8", "data": "synthetic", "dry_run": True,
+                          "config": {"workload": "dry run: 512x512 u8 erode 15x15 per rank through the CPU oracle"}}))
+    dist.close()
+    return 0
 
 
 def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     args = parse_args(argv)
+    rc = maybe_spawn(args, argv)
+    if rc is not None:
+        return rc
     dist = Dist()
+    if args.dry_run:
+        return run_dry(args, dist)
     if args.impl == "reference":
         return run_reference_arm(args, dist)
 
@@ -635,9 +802,21 @@ def main(argv=None):
     ms_per_step = max_ms / args.steps
     value = dist.world * wl.out_pixels_per_step() * args.steps / (max_ms / 1e3) / 1e9
 
+    # the timed steps' outputs, bit-exact against the CPU reference (outside the timed region,
+    # before the per-operation timings below overwrite the buffers)
+    check = None
+    if dist.rank == 0 and not args.no_self_check and hasattr(wl, "self_check"):
+        check = wl.self_check()
+
+    def family(label, spec) -> str:
+        if wl.name in ("cfg1", "cfg2"):
+            return pkg.plan_name(1, wl.img.shape[1], wl.img.shape[0], spec[0], spec[1], spec[2]).split("_")[0]
+        return label.split(" ")[0] if wl.name != "cfg3" else ("tiles" if "tiles" in label else "image")
+
     # per-operation durations: a graph of NB launches of one operation over all rotating buffers
     per_window = []
     tot_b = tot_t = 0.0
+    fam_b, fam_t, fam_ops = {}, {}, {}
     for (label, spec, nbytes, npx) in wl.ops:
         nb = getattr(wl, "NB", 1) if graphs else 3
         wl.cursor = 0
@@ -667,16 +846,33 @@ def main(argv=None):
         ms = e0.elapsed_time(e1) / n
         tot_b += nbytes
         tot_t += ms
-        per_window.append({"op": label, "us": round(ms * 1e3, 2), "gpix_s": round(npx / (ms / 1e3) / 1e9, 1),
-                           "gb_s": round(nbytes / (ms / 1e3) / 1e9, 1),
+        fam = family(label, spec)
+        fam_b[fam] = fam_b.get(fam, 0) + nbytes
+        fam_t[fam] = fam_t.get(fam, 0) + ms
+        fam_ops.setdefault(fam, []).append(label)
+        per_window.append({"op": label, "kernel": fam, "us": round(ms * 1e3, 2),
+                           "gpix_s": round(npx / (ms / 1e3) / 1e9, 1), "gb_s": round(nbytes / (ms / 1e3) / 1e9, 1),
                            "frac": round(nbytes / (ms / 1e3) / 1e9 / peak, 3)})
-    achieved = tot_b / (tot_t / 1e3) / 1e9
+    # roofline of the dominant kernel: the family with the largest share of the per-operation
+    # device time; achieved = its algorithmic bytes / its device time (CUDA events, serial)
+    dom = max(fam_t, key=fam_t.get)
+    achieved = fam_b[dom] / (fam_t[dom] / 1e3) / 1e9
+    step_bytes = sum(o[2] for o in wl.ops)
+    step_gbs = dist.world * step_bytes / (ms_per_step / 1e3) / 1e9
 
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{wl.name}.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch")
+            tj = json.load(open(tpath))
+            per_op = tj.get("per_op") or {}
+            vals = [per_op[lab]["dram_bytes"] for lab in fam_ops[dom] if lab in per_op]
+            if vals:
+                traffic = sum(vals) / len(vals)
+                traffic_src = f"{tpath[len(ROOT) + 1:]}: ncu dram__bytes_read+write per op, mean over {len(vals)} ops"
+            elif tj.get("bytes_per_launch"):
+                traffic = tj["bytes_per_launch"]
+                traffic_src = tpath[len(ROOT) + 1:]
         except Exception:
             traffic = None
 
@@ -706,13 +902,24 @@ def main(argv=None):
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": wl.dtype,
                 "data": "synthetic (seeded counter-based generator, SURVEY.md 8d; no dataset named)",
-                "config": dict(wl.config(), launch=(f"one CUDA graph per step ({glaunch} kernel nodes, the step's independent "
-                                                   f"operations forked over {args.streams} streams)") if graphs else "eager"),
+                "config": wl.config(),
+                "launch": (f"one CUDA graph per step ({glaunch} kernel nodes, the step's independent operations "
+                           f"forked over {args.streams} streams)") if graphs else "eager",
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": traffic,
-                             "kernel": "fused separable morph (all launches of the step)",
-                             "algorithmic_bytes": "1 read + 1 write per output pixel",
-                             "peak_source": peak_src},
+                             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                             "kernel": f"{dom}: " + ", ".join(fam_ops[dom]),
+                             "kernel_share_of_op_time": round(fam_t[dom] / tot_t, 3),
+                             "how": "algorithmic bytes of the dominant kernel family's operations / their device "
+                                    "time, each operation timed alone (CUDA events over a graph of launches)",
+                             "algorithmic_bytes": "1 read + 1 write per output pixel (per element for transposes)",
+                             "peak_source": peak_src,
+                             "step": {"achieved": step_gbs, "frac": step_gbs / peak,
+                                      "how": "all operations of the timed step (algorithmic bytes x ranks) / "
+                                             "ms_per_step"},
+                             "families": {f: {"achieved": fam_b[f] / (fam_t[f] / 1e3) / 1e9,
+                                              "frac": fam_b[f] / (fam_t[f] / 1e3) / 1e9 / peak,
+                                              "ops": len(fam_ops[f])} for f in fam_t}},
+                "self_check": check,
                 "per_window": per_window,
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
                 "plans": {lab: pkg.plan_name(1, 4096, 4096, spec[0], spec[1], spec[2]) for lab, spec, _, _ in wl.ops}

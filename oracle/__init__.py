@@ -174,6 +174,8 @@ class Reference:
         L.rmref_transpose_tiles_u16.argtypes = [_P, _S, _I, _I]
         L.rmref_calibrate.argtypes = [_I, _I, C.POINTER(C.c_int), _I, _I, C.POINTER(C.c_int),
                                       C.POINTER(C.c_int)]
+        L.rmref_set_pinning.argtypes = [_I]
+        L.rmref_set_pinning.restype = None
 
     @staticmethod
     def available(path: str = REF_SO) -> bool:
@@ -252,6 +254,10 @@ class Reference:
             self.lib.rmref_transpose_tiles_u16
         self._check(fn(_ptr(t), t.size // (n * n), n, nthreads), "rmref_transpose_tiles")
         return t
+
+    def set_pinning(self, on: bool) -> None:
+        """Pin band worker t to host CPU t (bench.py's timed CPU baseline)."""
+        self.lib.rmref_set_pinning(1 if on else 0)
 
     def calibrate(self, w, h, windows, reps):
         arr = (C.c_int * len(windows))(*windows)

@@ -21,6 +21,9 @@
 #include <thread>
 #include <vector>
 
+#include <pthread.h>
+#include <sched.h>
+
 #include "rectmorph/dispatch.hpp"
 #include "rectmorph/reference.hpp"
 #include "rectmorph/separable.hpp"
@@ -32,6 +35,29 @@ using namespace rectmorph;
 #define RMREF_API extern "C" __attribute__((visibility("default")))
 
 namespace {
+
+// bench.py's CPU baseline pins worker t to host CPU t (of the process's allowed CPUs) so the
+// median of repetitions is not shuffled by the scheduler (timing.hpp:22-53 times one thread)
+int g_pin = 0;
+void pin_self(int t) {
+    if (!g_pin) return;
+    cpu_set_t allowed;
+    CPU_ZERO(&allowed);
+    if (sched_getaffinity(0, sizeof allowed, &allowed) != 0) return;
+    const int n = CPU_COUNT(&allowed);
+    if (n <= 0) return;
+    int k = t % n, cpu = -1;
+    for (int c = 0; c < CPU_SETSIZE; ++c)
+        if (CPU_ISSET(c, &allowed) && k-- == 0) {
+            cpu = c;
+            break;
+        }
+    if (cpu < 0) return;
+    cpu_set_t one;
+    CPU_ZERO(&one);
+    CPU_SET(cpu, &one);
+    pthread_setaffinity_np(pthread_self(), sizeof one, &one);
+}
 
 int map_error(const Error& e) { return int(e.code()) + 1; }
 
@@ -97,6 +123,7 @@ RMREF_API int rmref_morph_u8(const std::uint8_t* src, std::size_t sstride, int w
         std::vector<int> status(std::size_t(nt), 0);
         for (int t = 0; t < nt; ++t) {
             pool.emplace_back([&, t] {
+                pin_self(t);
                 const int r0 = int((long long)h * t / nt), r1 = int((long long)h * (t + 1) / nt);
                 const int a = std::max(0, r0 - halo), z = std::min(h, r1 + halo);
                 try {
@@ -180,6 +207,7 @@ RMREF_API int rmref_transpose_image_u8(const std::uint8_t* src, std::size_t sstr
         std::vector<std::thread> pool;
         for (int k = 0; k < nt; ++k) {
             pool.emplace_back([&, k] {
+                pin_self(k);
                 int r0 = int((long long)h * k / nt), r1 = int((long long)h * (k + 1) / nt);
                 r0 &= ~15;
                 if (k + 1 < nt) r1 &= ~15; else r1 = h;
@@ -212,6 +240,7 @@ static int tiles_impl(T* data, std::size_t n_tiles, int n, int nthreads) {
         std::vector<std::thread> pool;
         for (int k = 0; k < nt; ++k)
             pool.emplace_back([&, k] {
+                pin_self(k);
                 const std::size_t a = n_tiles * std::size_t(k) / std::size_t(nt);
                 const std::size_t z = n_tiles * std::size_t(k + 1) / std::size_t(nt);
                 for (std::size_t i = a; i < z; ++i) transpose_tile(data + i * tile, std::size_t(n), n);
@@ -236,3 +265,5 @@ RMREF_API int rmref_calibrate(int w, int h, const int* windows, int n_windows, i
         *threshold_v = c.threshold_v;
     });
 }
+
+RMREF_API void rmref_set_pinning(int on) { g_pin = on; }
