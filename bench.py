@@ -493,12 +493,18 @@ class Cfg3:
         import paper_2002_09474_b200 as pkg
         self.pkg = pkg
         n = 8192
-        self.a8 = torch.empty((n, n), dtype=torch.uint8, device="cuda")
-        self.a16 = torch.empty((n, n), dtype=torch.uint16, device="cuda")
-        pkg.generate_device(self.a8, 3)
-        pkg.generate_device(self.a16, 30)
-        self.t8 = torch.empty_like(self.a8)
-        self.t16 = torch.empty_like(self.a16)
+        # 4 rotating u8 pairs (512 MiB) and 2 u16 pairs (512 MiB): no image transpose re-reads its
+        # input or output from the 126 MB L2
+        self.a8s = [torch.empty((n, n), dtype=torch.uint8, device="cuda") for _ in range(4)]
+        self.a16s = [torch.empty((n, n), dtype=torch.uint16, device="cuda") for _ in range(2)]
+        for a in self.a8s:
+            pkg.generate_device(a, 3)
+        for a in self.a16s:
+            pkg.generate_device(a, 30)
+        self.t8s = [torch.empty_like(a) for a in self.a8s]
+        self.t16s = [torch.empty_like(a) for a in self.a16s]
+        self.a8, self.a16, self.t8, self.t16 = self.a8s[0], self.a16s[0], self.t8s[0], self.t16s[0]
+        self.k8 = self.k16 = 0
         self.tiles8 = torch.empty((1 << 24) * 64, dtype=torch.uint8, device="cuda")
         self.tiles16 = torch.empty((1 << 24) * 256, dtype=torch.uint8, device="cuda")
         pkg.generate_device(self.tiles8.view(1 << 14, -1), 31)
@@ -511,9 +517,13 @@ class Cfg3:
 
     def launch(self, spec):
         if spec == "t8":
-            self.pkg.transpose_device(self.a8, self.t8)
+            i = self.k8 % len(self.a8s)
+            self.k8 += 1
+            self.pkg.transpose_device(self.a8s[i], self.t8s[i])
         elif spec == "t16":
-            self.pkg.transpose_device(self.a16, self.t16)
+            i = self.k16 % len(self.a16s)
+            self.k16 += 1
+            self.pkg.transpose_device(self.a16s[i], self.t16s[i])
         elif spec == "k8":
             self.pkg.transpose_tiles_device(self.tiles8, 8)
         else:
@@ -524,21 +534,24 @@ class Cfg3:
         by the timed steps (in place), so they must equal their generator input again; plus one
         extra call checked per element against the closed form."""
         import torch
-        ok = bool(torch.equal(self.t8, self.a8.t().contiguous()))
-        ok &= bool(torch.equal(self.t16.view(torch.uint8).view(8192, 8192, 2),
-                               self.a16.view(torch.uint8).view(8192, 8192, 2).transpose(0, 1).contiguous()))
+        torch.cuda.synchronize()
+        ok = all(bool(torch.equal(t, a.t().contiguous())) for a, t in zip(self.a8s, self.t8s))
+        ok &= all(bool(torch.equal(t.view(torch.uint8).view(8192, 8192, 2),
+                                   a.view(torch.uint8).view(8192, 8192, 2).transpose(0, 1).contiguous()))
+                  for a, t in zip(self.a16s, self.t16s))
         for t, n in ((self.tiles8, 8), (self.tiles16, 16)):
             before = t.view(-1, n, n)[:1 << 16].transpose(1, 2).contiguous()
             self.pkg.transpose_tiles_device(t, n)
             torch.cuda.synchronize()
             ok &= bool(torch.equal(t.view(-1, n, n)[:1 << 16], before))
             self.pkg.transpose_tiles_device(t, n)  # back
-        return {"bit_exact": ok, "checked": "both 8192^2 images (all elements); 2^16 tiles of each size",
+        return {"bit_exact": ok, "checked": "every rotating 8192^2 image pair (all elements); 2^16 tiles of each size",
                 "against": "closed form (x^T)"}
 
     def config(self):
         return {"workload": "cfg3: transpose 8192^2 u8 + 8192^2 u16, 2^24 8x8 + 2^24 16x16 u8 tiles in place",
-                "unit_note": "value counts transposed elements (Gelem/s)", "l2": "no flush: buffers >> L2",
+                "unit_note": "value counts transposed elements (Gelem/s)",
+                "l2": "no flush: 4 rotating u8 and 2 u16 image pairs (512 MiB each), 1 / 4 GiB tile arrays >> L2",
                 "parallelism": f"replicas x{self.dist.world}"}
 
     def out_pixels_per_step(self):

@@ -17,6 +17,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <stdexcept>
+#include <iosfwd>
 #include <string>
 #include <vector>
 
@@ -184,6 +185,17 @@ void transpose_tile(std::uint16_t* data, std::size_t stride, int n);
 void transpose_tile(std::uint32_t* data, std::size_t stride, int n);
 Image transpose_image(const Image& src);
 Image16 transpose_image(const Image16& src);
+
+// ---- PGM files (reference pgm.hpp:10-24) -------------------------------------------------------
+// P5 (binary) and P2 (ASCII) with maxval 255; '#' comments anywhere in the header and, for P2,
+// between pixel tokens. Errors: Errc::BadMagic, BadHeader (malformed header, extents outside
+// 1..2^20, P2 token > 255 or not a number), UnsupportedMaxval, TruncatedData, IoError (files,
+// message names the path), BadArgument (writing an empty image). Writes are canonical:
+// "P5\n<w> <h>\n255\n" + rows, or P2 with one image row per text line; never comments.
+Image read_pgm(std::istream& in);
+void write_pgm(std::ostream& out, const Image& img, bool binary = true);
+Image load_pgm(const std::string& path);
+void store_pgm(const std::string& path, const Image& img, bool binary = true);
 
 // ---- 1-D API (reference sliding_extrema.hpp:11-44) ----------------------------------------------
 struct OpCounter {

@@ -340,6 +340,103 @@ def van_herk_1d(sig, window, op, border=BorderPolicy(), counter=None):
 
 
 # ------------------------------------------------------------------------------------------
+# PGM files (pgm.hpp:10-24): host-side format code, the same rules as the C++ drop-in
+# ------------------------------------------------------------------------------------------
+_PGM_MAX_SIDE = 1 << 20
+
+
+def read_pgm(data: bytes) -> np.ndarray:
+    """P5 / P2, maxval 255, '#' comments in the header (and between P2 tokens)."""
+    pos = 0
+    n = len(data)
+
+    def to_token() -> bool:
+        nonlocal pos
+        while pos < n:
+            c = data[pos]
+            if c == 0x23:  # '#': to the end of the line
+                while pos < n and data[pos] != 0x0A:
+                    pos += 1
+            elif c in b" \t\n\r\v\f":
+                pos += 1
+            else:
+                return True
+        return False
+
+    def token(what: str, at_eof: Errc) -> int:
+        nonlocal pos
+        if not to_token():
+            raise Error(at_eof, f"stream ended before the {what}")
+        if not 0x30 <= data[pos] <= 0x39:
+            raise Error(Errc.BadHeader, f"the {what} is not a number")
+        v = 0
+        while pos < n and 0x30 <= data[pos] <= 0x39:
+            v = v * 10 + data[pos] - 0x30
+            pos += 1
+            if v > 100 * _PGM_MAX_SIDE:
+                raise Error(Errc.BadHeader, f"the {what} is out of range")
+        return v
+
+    if n < 2 or data[0] != 0x50 or data[1] not in (0x35, 0x32):
+        raise Error(Errc.BadMagic, "not a P5 / P2 PGM stream")
+    binary = data[1] == 0x35
+    pos = 2
+    w, h = token("width", Errc.BadHeader), token("height", Errc.BadHeader)
+    if not (1 <= w <= _PGM_MAX_SIDE and 1 <= h <= _PGM_MAX_SIDE):
+        raise Error(Errc.BadHeader, "image extents out of range")
+    if token("maxval", Errc.BadHeader) != 255:
+        raise Error(Errc.UnsupportedMaxval, "maxval must be 255")
+    if binary:
+        if pos >= n or data[pos] not in b" \t\n\r\v\f":
+            raise Error(Errc.BadHeader, "no whitespace after the maxval")
+        pos += 1
+        if n - pos < w * h:
+            raise Error(Errc.TruncatedData, "pixel data ends early")
+        return np.frombuffer(data, np.uint8, w * h, pos).reshape(h, w).copy()
+    out = np.empty((h, w), np.uint8)
+    for i in range(w * h):
+        v = token("pixel", Errc.TruncatedData)
+        if v > 255:
+            raise Error(Errc.BadHeader, "a pixel exceeds the maxval")
+        out.flat[i] = v
+    return out
+
+
+def write_pgm(img: np.ndarray, binary: bool = True) -> bytes:
+    img = np.asarray(img)
+    if img.ndim != 2 or img.dtype != np.uint8:
+        raise Error(Errc.BadArgument, "expected a 2-D uint8 image")
+    if img.size == 0:
+        raise Error(Errc.BadArgument, "an empty image has no PGM form")
+    h, w = img.shape
+    head = f"{'P5' if binary else 'P2'}\n{w} {h}\n255\n".encode()
+    if binary:
+        return head + np.ascontiguousarray(img).tobytes()
+    return head + "".join(" ".join(str(int(v)) for v in row) + "\n" for row in img).encode()
+
+
+def load_pgm(path: str) -> np.ndarray:
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise Error(Errc.IoError, f"cannot open '{path}'") from None
+    try:
+        return read_pgm(data)
+    except Error as e:
+        raise Error(e.code, f"{path}: {e}") from None
+
+
+def store_pgm(path: str, img: np.ndarray, binary: bool = True) -> None:
+    data = write_pgm(img, binary)
+    try:
+        with open(path, "wb") as f:
+            f.write(data)
+    except OSError:
+        raise Error(Errc.IoError, f"cannot open '{path}' for writing") from None
+
+
+# ------------------------------------------------------------------------------------------
 # device level (torch CUDA tensors); pitch = tensor.stride(0) * itemsize
 # ------------------------------------------------------------------------------------------
 def _dev(t):

@@ -20,6 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "librmgpu.so")
 HOSTLIB = os.path.join(PKG, "librectmorph_b200.so")
+CLI = os.path.join(PKG, "rectmorph_b200")  # the reference CLI (apply | bench | calibrate) on the GPU
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -27,8 +28,7 @@ NVCC_FLAGS = ARCH + (["-DRMGPU_TRACE"] if os.environ.get("RMGPU_TRACE") else [])
     os.environ.get("RMGPU_EXTRA_DEFS", "").split() + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
                      "-I", os.path.join(ROOT, "include")]
-CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_fast.cu", "morph_fast_u8_min.cu", "morph_fast_u8_max.cu",
-              "morph_fast_u16_min.cu", "morph_fast_u16_max.cu", "morph_stream.cu", "morph_phase.cu",
+CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_stream.cu", "morph_phase.cu",
               "morph_phase_u8_min.cu", "morph_phase_u8_max.cu", "morph_phase_u16_min.cu", "morph_phase_u16_max.cu",
               "morph_col.cu", "morph_col_u8_min.cu", "morph_col_u8_max.cu", "morph_col_u16_min.cu",
               "morph_col_u16_max.cu", "morph_col_u8_grad.cu", "morph_col_u16_grad.cu", "morph_sep.cu",
@@ -37,7 +37,7 @@ CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_fast.cu", "morph_fast_u8_min
               "generate.cu", "morph_fuse.cu"]
 # K4 instantiations: morph_fuse_inst.cu compiled once per (pixel size, mode, block size B)
 FUSE_VARIANTS = [(sz, mx, b) for sz in (1, 2) for mx in (0, 1) for b in ((8, 12, 16, 20, 24) if sz == 1 else (8, 12, 16))]
-HOST_SOURCES = [os.path.join("host", "rectmorph_b200.cpp")]
+HOST_SOURCES = [os.path.join("host", "rectmorph_b200.cpp"), os.path.join("host", "pgm_b200.cpp")]
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -111,8 +111,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or _newer(HOSTLIB, host_srcs + [host_hdr, LIB, os.path.join(ROOT, "include", "rmgpu.h")]):
         _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
               "-o", HOSTLIB] + host_srcs + ["-L", PKG, "-lrmgpu", "-Wl,-rpath,$ORIGIN"])
+    cli_src = os.path.join(CSRC, "host", "rectmorph_cli_b200.cpp")
+    if force or _newer(CLI, [cli_src, host_hdr, HOSTLIB, LIB, os.path.join(ROOT, "include", "rmgpu.h")]):
+        _run(["g++", "-O2", "-std=c++20", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+              "-o", CLI, cli_src, "-L", PKG, "-lrectmorph_b200", "-lrmgpu", "-L", "/usr/local/cuda/lib64", "-lcudart",
+              "-Wl,-rpath,$ORIGIN", "-Wl,-rpath,/usr/local/cuda/lib64"])
     if verbose:
-        print("built", LIB, HOSTLIB)
+        print("built", LIB, HOSTLIB, CLI)
     return LIB
 
 

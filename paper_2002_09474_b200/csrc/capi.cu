@@ -236,6 +236,45 @@ int run_single(MorphJob j) {
         return RMGPU_OK;
     }
     cudaError_t e = cudaSuccess;
+    // Pitches / pointers that are not 16-byte aligned (the reference pads rows to 16 bytes,
+    // image.cpp:9-14, so only foreign layouts hit this): stage through aligned scratch copies
+    // (one 2-D copy in, one out) and run the TMA / vectorised kernels on those, instead of
+    // scalar fallback kernels.
+    {
+        const uintptr_t s0 = reinterpret_cast<uintptr_t>(j.src) - (uintptr_t)((ptrdiff_t)j.above * (ptrdiff_t)j.sp);
+        const bool al = ((s0 | reinterpret_cast<uintptr_t>(j.dst) | j.sp | j.dp | (j.batch > 1 ? (j.simg | j.dimg) : 0)) &
+                         15) == 0;
+        if (!al && !g_disable_stream) {
+            const size_t rb = (size_t)j.W * j.elem, tp = (rb + 255) & ~size_t(255);
+            const int rin = j.above + j.H + j.below;
+            const size_t simg = tp * (size_t)rin, dimg = tp * (size_t)j.H;
+            char* buf = nullptr;
+            RM_CUDA(scratch_alloc(reinterpret_cast<void**>(&buf), (simg + dimg) * (size_t)j.batch, j.stream));
+            int rc = RMGPU_OK;
+            for (int b = 0; rc == RMGPU_OK && b < j.batch; ++b) {
+                e = cudaMemcpy2DAsync(buf + b * simg, tp, reinterpret_cast<const char*>(s0) + (size_t)b * j.simg, j.sp, rb,
+                                      rin, cudaMemcpyDeviceToDevice, j.stream);
+                if (e != cudaSuccess) rc = cuda_fail(e, "staging copy in");
+            }
+            MorphJob k = j;
+            k.src = buf + (size_t)j.above * tp;
+            k.sp = tp;
+            k.simg = simg;
+            k.dst = buf + simg * (size_t)j.batch;
+            k.dp = tp;
+            k.dimg = dimg;
+            if (rc == RMGPU_OK) rc = run_single(k);
+            for (int b = 0; rc == RMGPU_OK && b < j.batch; ++b) {
+                e = cudaMemcpy2DAsync(static_cast<char*>(j.dst) + (size_t)b * j.dimg, j.dp,
+                                      static_cast<char*>(k.dst) + b * dimg, tp, rb, j.H, cudaMemcpyDeviceToDevice,
+                                      j.stream);
+                if (e != cudaSuccess) rc = cuda_fail(e, "staging copy out");
+            }
+            cudaError_t fe = cudaFreeAsync(buf, j.stream);
+            if (rc == RMGPU_OK && fe != cudaSuccess) rc = cuda_fail(fe, "cudaFreeAsync");
+            return rc;
+        }
+    }
     // Explicit algorithm hints (rmgpu.h): Linear on an axis whose wing is >= 4 runs that axis as a
     // direct sliding window (generic pass kernel), the other axis through the planner, via one
     // intermediate; everything else (Auto, VanHerk, Linear on short wings -- where the planner's
@@ -357,10 +396,6 @@ int run_single(MorphJob j) {
         }
     }
 gradient_fallback:
-    if (rmgpu::launch_fast(j, &e)) {
-        if (e != cudaSuccess) return cuda_fail(e, "fast morph kernel");
-        return RMGPU_OK;
-    }
     if (rmgpu::generic_tile_fits(j)) {
         e = rmgpu::launch_generic_tile(j);
         if (e != cudaSuccess) return cuda_fail(e, "generic morph kernel");
@@ -864,7 +899,6 @@ const char* rmgpu_plan_name(int elem_bytes, int width, int height, int wx, int w
             return g.c_str();
         }
     }
-    if (const char* n = rmgpu::fast_plan_name(j)) return n;
     if (rmgpu::generic_tile_fits(j)) return "generic_tile";
     return "two_pass_global";
 }

@@ -46,11 +46,6 @@ cudaError_t launch_pass_cols(const MorphJob& j);
 cudaError_t launch_subtract(const void* a, size_t ap, const void* b, size_t bp, void* dst,
                             size_t dp, int W, int H, int elem, cudaStream_t s);
 
-// ---- fast fused separable path (morph_fast.cu) -----------------------------------------------
-// Returns true and launches when a specialised kernel covers the job; false = caller falls back.
-bool launch_fast(const MorphJob& j, cudaError_t* err);
-const char* fast_plan_name(const MorphJob& j);
-
 // ---- shared TMA infrastructure (morph_stream.cu) -----------------------------------------------
 namespace stream {
 void set_trace(long long* device_buf, int cta);  // debug timeline of the phase kernel (tools/trace_phase.py)

@@ -1,12 +1,14 @@
 // morph_generic.cu -- generic (any window, any pitch) GPU paths.
 //
-// These are the fallbacks behind the specialised fused kernels in morph_fast.cu:
+// The fallbacks behind the TMA kernels (K1 / K3 / K2), reached only when those decline a job
+// (RMGPU_DISABLE_STREAM, windows beyond their register budgets); unaligned pitches are staged
+// into aligned scratch and go to the TMA kernels instead (capi.cu run_single):
 //   * morph_generic_tile: one fused kernel, input tile + halo staged in shared memory with the
 //     border rule resolved at load time (image.cpp:58-66), vertical then horizontal pass
-//     (separable.cpp:141-145) as direct window loops. Used when no fast variant covers the
-//     window / dtype, and as an independent second GPU implementation in the tests.
-//   * pass_rows / pass_cols: single 1-D passes straight from global memory, for windows too
-//     large for a shared-memory tile and for the pass-level API (separable.hpp:20-37).
+//     (separable.cpp:141-145) as direct window loops.
+//   * pass_rows / pass_cols: single 1-D direct passes straight from global memory, for windows
+//     too large for a shared-memory tile, and the direct sliding window an explicit Linear
+//     algorithm hint asks for on a long wing (rmgpu.h).
 #include "common.cuh"
 #include "kernels.h"
 

@@ -171,9 +171,6 @@ transpose_image_bfly_kernel(const T* __restrict__ src, size_t sp, T* __restrict_
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// K5: batched tile transposes, one tile per thread (contiguous tiles)
-// ------------------------------------------------------------------------------------------
 // 4x4 byte transpose of four row words a[0..3] -> column words b[0..3].
 __device__ __forceinline__ void t4x4_u8(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                         uint32_t& b0, uint32_t& b1, uint32_t& b2, uint32_t& b3) {
@@ -184,6 +181,72 @@ __device__ __forceinline__ void t4x4_u8(uint32_t a0, uint32_t a1, uint32_t a2, u
     b2 = prmt(t1, t3, 0x5410);
     b3 = prmt(t1, t3, 0x7632);
 }
+
+// Image transpose, full tiles, block version (replaces the shuffle butterfly, which ncu showed
+// MIO-throttled: 16 SHFL per 16 bytes). A CTA stages TH input rows x 128 bytes in shared memory
+// (coalesced 128-bit loads, 8-byte chunks XOR-swizzled by row block so the column-block reads are
+// conflict-free); each thread then reads one 8x8 u8 / 4x4 u16 block with 64-bit shared loads,
+// transposes it in registers with byte / half-word permutes and writes it as 8 / 4 output row
+// pieces of 8 bytes -- the 16 lanes of a half warp cover 128 contiguous bytes of an output row.
+template <typename T>
+__global__ void __launch_bounds__(256)
+transpose_image_blk_kernel(const T* __restrict__ src, size_t sp, T* __restrict__ dst, size_t dp) {
+    constexpr int ELEM = sizeof(T);
+    constexpr int BR = ELEM == 1 ? 8 : 4;        // block rows (8x8 u8, 4x4 u16: 8 bytes per row)
+    constexpr int TH = 16 * BR;                  // tile rows (16 row blocks)
+    constexpr int RB = 128;                      // tile row bytes (16 chunks of 8 bytes)
+    constexpr int TX = RB / ELEM;                // tile columns
+    __shared__ __align__(16) unsigned char tile[TH * RB];
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TH;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned char* s8 = reinterpret_cast<const unsigned char*>(src);
+    unsigned char* d8 = reinterpret_cast<unsigned char*>(dst);
+    constexpr int LPT = TH * RB / 16 / 256;      // 16-byte loads per thread (4 u8, 2 u16)
+    uint4 v[LPT];
+#pragma unroll
+    for (int k = 0; k < LPT; ++k) {
+        const int c = tid + 256 * k, r = c >> 3, q = c & 7;  // row, 16-byte chunk
+        v[k] = __ldcs(reinterpret_cast<const uint4*>(s8 + (size_t)(y0 + r) * sp + (size_t)x0 * ELEM + q * 16));
+    }
+#pragma unroll
+    for (int k = 0; k < LPT; ++k) {
+        const int c = tid + 256 * k, r = c >> 3, q = c & 7;
+        const int sw = (r / BR) & 15;            // 8-byte chunk 2q / 2q+1 -> (2q) ^ sw / (2q+1) ^ sw
+        const int p = (2 * q) ^ sw;
+        const uint4 w = (p & 1) ? make_uint4(v[k].z, v[k].w, v[k].x, v[k].y) : v[k];
+        *reinterpret_cast<uint4*>(tile + r * RB + (p & ~1) * 8) = w;
+    }
+    __syncthreads();
+    const int by = lane & 15, bx = warp * 2 + (lane >> 4);  // row block, 8-byte column block
+    uint2 r[BR];
+#pragma unroll
+    for (int i = 0; i < BR; ++i)
+        r[i] = *reinterpret_cast<const uint2*>(tile + (by * BR + i) * RB + ((bx ^ by) * 8));
+    // output row o (input column x0 + bx * (8 / ELEM) + o) gets this block's BR rows
+    unsigned char* drow = d8 + (size_t)(x0 + bx * (8 / ELEM)) * dp + (size_t)(y0 + by * BR) * ELEM;
+    if constexpr (ELEM == 1) {
+        uint32_t lo[8], hi[8];
+        t4x4_u8(r[0].x, r[1].x, r[2].x, r[3].x, lo[0], lo[1], lo[2], lo[3]);
+        t4x4_u8(r[0].y, r[1].y, r[2].y, r[3].y, lo[4], lo[5], lo[6], lo[7]);
+        t4x4_u8(r[4].x, r[5].x, r[6].x, r[7].x, hi[0], hi[1], hi[2], hi[3]);
+        t4x4_u8(r[4].y, r[5].y, r[6].y, r[7].y, hi[4], hi[5], hi[6], hi[7]);
+#pragma unroll
+        for (int o = 0; o < 8; ++o) __stcs(reinterpret_cast<uint2*>(drow + (size_t)o * dp), make_uint2(lo[o], hi[o]));
+    } else {
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int wi = o >> 1;
+            const uint32_t sel = (o & 1) ? 0x7632u : 0x5410u;
+            const uint32_t a0 = wi ? r[0].y : r[0].x, a1 = wi ? r[1].y : r[1].x;
+            const uint32_t a2 = wi ? r[2].y : r[2].x, a3 = wi ? r[3].y : r[3].x;
+            __stcs(reinterpret_cast<uint2*>(drow + (size_t)o * dp), make_uint2(prmt(a0, a1, sel), prmt(a2, a3, sel)));
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K5: batched tile transposes, one tile per thread (contiguous tiles)
+// ------------------------------------------------------------------------------------------
 
 // u8 tile of side N (4, 8, 16): N rows x N/4 words.
 template <int N>
@@ -266,14 +329,23 @@ tiles_generic_kernel(T* __restrict__ data, size_t n_tiles, int n, size_t row_str
 cudaError_t launch_transpose(const void* src, size_t sp, void* dst, size_t dp, int W, int H, int elem,
                              cudaStream_t s) {
     const int vec_ok = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | sp | dp) & 15) == 0;
-    const int TX = 256 / elem;  // butterfly tile: 64 rows x 256 bytes
-    const int FW = vec_ok ? W / TX * TX : 0, FH = vec_ok ? H / kTT * kTT : 0;  // full-tile region
+    const bool bfly = tune("transpose_bfly", 0) != 0;  // the earlier shuffle-butterfly kernel
+    const int TX = bfly ? 256 / elem : 128 / elem;            // full tile: columns x rows
+    const int TY = bfly ? kTT : (elem == 1 ? 128 : 64);
+    const int FW = vec_ok ? W / TX * TX : 0, FH = vec_ok ? H / TY * TY : 0;  // full-tile region
     if (FW && FH) {
-        dim3 grid(FW / TX, FH / kTT);
-        if (elem == 1)
-            transpose_image_bfly_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)src, sp, (uint8_t*)dst, dp, W, H);
-        else
-            transpose_image_bfly_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)src, sp, (uint16_t*)dst, dp, W, H);
+        dim3 grid(FW / TX, FH / TY);
+        if (bfly) {
+            if (elem == 1)
+                transpose_image_bfly_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)src, sp, (uint8_t*)dst, dp, W, H);
+            else
+                transpose_image_bfly_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)src, sp, (uint16_t*)dst, dp, W,
+                                                                          H);
+        } else if (elem == 1) {
+            transpose_image_blk_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)src, sp, (uint8_t*)dst, dp);
+        } else {
+            transpose_image_blk_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)src, sp, (uint16_t*)dst, dp);
+        }
         count_launch();
     }
     // ragged right columns / bottom rows (and unaligned images): the shared-memory tile kernel
