@@ -573,6 +573,86 @@ struct DevBuf {
     ~DevBuf() { if (p) cudaFreeAsync(p, s); }
 };
 
+// The band pipeline of one host call, enqueued on `s` (+ the thread's `up` / `down` copy streams,
+// forked from and joined back into `s`): band k uploads on `up` as two copies -- its first `halo`
+// rows (what band k-1 needs below it) and the rest -- and is computed on `s` once it and the first
+// rows of band k+1 have arrived; its result downloads on `down` while later bands still upload, so
+// the two copy directions overlap each other and the kernels. The scratch images are allocated and
+// freed on `s`.
+int enqueue_host_pipeline(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int wx, int wy,
+                          int op, int border, unsigned bval, int elem, int algo_h, int algo_v, size_t pitch, int R,
+                          int nb, int halo, cudaStream_t s) {
+    int rc;
+    const size_t rb = (size_t)W * elem;
+    if ((rc = host_events(3 * (size_t)nb + 2))) return rc;
+    cudaEvent_t* ev_head = t_ctx.events.data();   // band k's first `halo` rows uploaded
+    cudaEvent_t* ev_band = ev_head + nb;          // band k uploaded
+    cudaEvent_t* ev_out = ev_band + nb;           // band k computed
+    cudaEvent_t ev_start = ev_out[nb], ev_end = ev_out[nb + 1];
+    char *a = nullptr, *b = nullptr;
+    RM_CUDA(scratch_alloc(reinterpret_cast<void**>(&a), pitch * H, s));
+    RM_CUDA(scratch_alloc(reinterpret_cast<void**>(&b), pitch * H, s));
+    RM_CUDA(cudaEventRecord(ev_start, s));
+    RM_CUDA(cudaStreamWaitEvent(t_ctx.up, ev_start, 0));
+    RM_CUDA(cudaStreamWaitEvent(t_ctx.down, ev_start, 0));
+    const bool flat_in = sp == rb && pitch == rb, flat_out = dp == rb && pitch == rb;
+    auto upload = [&](int r0, int n) -> cudaError_t {
+        char* d = a + (size_t)r0 * pitch;
+        const char* h = static_cast<const char*>(hsrc) + (size_t)r0 * sp;
+        return flat_in ? cudaMemcpyAsync(d, h, rb * n, cudaMemcpyHostToDevice, t_ctx.up)
+                       : cudaMemcpy2DAsync(d, pitch, h, sp, rb, n, cudaMemcpyHostToDevice, t_ctx.up);
+    };
+    for (int k = 0; k < nb; ++k) {
+        const int r0 = k * R, n = std::min(R, H - r0), head = std::min(n, halo);
+        if (head > 0 && head < n) RM_CUDA(upload(r0, head));
+        RM_CUDA(cudaEventRecord(ev_head[k], t_ctx.up));
+        RM_CUDA(upload(r0 + (head < n ? head : 0), head < n ? n - head : n));
+        RM_CUDA(cudaEventRecord(ev_band[k], t_ctx.up));
+    }
+    for (int k = 0; rc == RMGPU_OK && k < nb; ++k) {
+        const int r0 = k * R, n = std::min(R, H - r0);
+        RM_CUDA(cudaStreamWaitEvent(s, ev_band[k], 0));
+        if (k + 1 < nb) RM_CUDA(cudaStreamWaitEvent(s, ev_head[k + 1], 0));  // halo rows below
+        const int above = std::min(halo, r0), below = std::min(halo, H - r0 - n);
+        rc = run_morph(a + (size_t)r0 * pitch, pitch, 0, b + (size_t)r0 * pitch, pitch, 0, 1, W, n, above, below, wx,
+                       wy, op, border, bval, elem, s, algo_h, algo_v);
+        if (rc) break;
+        RM_CUDA(cudaEventRecord(ev_out[k], s));
+        RM_CUDA(cudaStreamWaitEvent(t_ctx.down, ev_out[k], 0));
+        char* h = static_cast<char*>(hdst) + (size_t)r0 * dp;
+        const char* d = b + (size_t)r0 * pitch;
+        if (flat_out) RM_CUDA(cudaMemcpyAsync(h, d, rb * n, cudaMemcpyDeviceToHost, t_ctx.down));
+        else RM_CUDA(cudaMemcpy2DAsync(h, dp, d, pitch, rb, n, cudaMemcpyDeviceToHost, t_ctx.down));
+    }
+    // join both copy streams back into `s` before the buffers go back to the pool
+    RM_CUDA(cudaEventRecord(ev_end, t_ctx.down));
+    RM_CUDA(cudaStreamWaitEvent(s, ev_end, 0));
+    RM_CUDA(cudaEventRecord(ev_start, t_ctx.up));
+    RM_CUDA(cudaStreamWaitEvent(s, ev_start, 0));
+    cudaError_t fa = cudaFreeAsync(a, s), fb = cudaFreeAsync(b, s);
+    if (rc) return rc;
+    if (fa != cudaSuccess) return cuda_fail(fa, "cudaFreeAsync");
+    if (fb != cudaSuccess) return cuda_fail(fb, "cudaFreeAsync");
+    return RMGPU_OK;
+}
+
+// Repeated host calls with the same arguments (a loop over frames, a benchmark) replay the whole
+// band pipeline as one CUDA graph: one launch instead of ~10 API calls per band, which lets the
+// pipeline use finer bands (shorter fill and drain) without becoming CPU-bound.
+struct HostGraphKey {
+    const void* hsrc;
+    void* hdst;
+    size_t sp, dp;
+    int W, H, wx, wy, op, border, elem, algo_h, algo_v, nb, dev;
+    unsigned bval;
+    bool operator==(const HostGraphKey& o) const { return memcmp(this, &o, sizeof o) == 0; }
+};
+struct HostGraphEntry {
+    HostGraphKey key;
+    cudaGraphExec_t exec;  // nullptr: capture not possible for this call, run it directly
+};
+thread_local std::vector<HostGraphEntry> t_graphs;
+
 int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int wx, int wy, int op,
                int border, unsigned bval, int elem, int algo_h, int algo_v) {
     int rc;
@@ -585,20 +665,21 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     // device rows as tight as the kernels allow (16-byte pitch): a host image whose rows are
     // already that tight then moves as one flat copy instead of a 2-D copy of H short rows
     const size_t rb = (size_t)W * elem, pitch = rb % 16 == 0 ? rb : (rb + 255) & ~size_t(255);
-    DevBuf a, b;
-    a.s = b.s = s;
-    RM_CUDA(scratch_alloc(&a.p, pitch * H, s));
-    RM_CUDA(scratch_alloc(&b.p, pitch * H, s));
-    // Pipelined over row bands: band k uploads on `up`, is computed on `stream` once the band below
-    // it has arrived too (its halo rows; bands are at least one halo tall), and downloads on `down`
-    // while later bands still upload -- the two copy directions overlap each other and the kernels.
     const int halo = (op == RMGPU_OPEN || op == RMGPU_CLOSE) ? 2 * (wy / 2) : wy / 2;
-    // 4096^2: 0.65 -> 0.56 ms per call (PCIe-bound); small images (1920x1080) lose more to the
-    // per-band API calls than they gain from the overlap
-    const int nb_target = rmgpu::tune("host_bands", rb * (size_t)H >= ((size_t)8 << 20) ? 6 : 1);
+    const bool big = rb * (size_t)H >= ((size_t)8 << 20);
+    const bool graphs = rmgpu::tune("host_graph", 1) != 0;
+    // bands (4096^2 u8, tools/e2e_probe.py): the fill (first band up) and drain (last band down)
+    // shrink with more bands but every copy has a fixed cost on the copy engines: 2-4 bands with the
+    // head rows uploaded separately measured best (0.52-0.56 ms per call; 6 bands 0.55-0.59,
+    // 16 bands 0.72; round 1's 6 bands without the head split 0.58)
+    const int nb_target = rmgpu::tune("host_bands", big ? 3 : 1);
     const int R = std::max({halo, 64, (H + nb_target - 1) / std::max(1, nb_target)});
     const int nb = (H + R - 1) / R;
     if (nb < 2) {
+        DevBuf a, b;
+        a.s = b.s = s;
+        RM_CUDA(scratch_alloc(&a.p, pitch * H, s));
+        RM_CUDA(scratch_alloc(&b.p, pitch * H, s));
         if (sp == rb && pitch == rb) RM_CUDA(cudaMemcpyAsync(a.p, hsrc, rb * H, cudaMemcpyHostToDevice, s));
         else RM_CUDA(cudaMemcpy2DAsync(a.p, pitch, hsrc, sp, rb, H, cudaMemcpyHostToDevice, s));
         rc = run_morph(a.p, pitch, 0, b.p, pitch, 0, 1, W, H, 0, 0, wx, wy, op, border, bval, elem, s, algo_h, algo_v);
@@ -608,53 +689,61 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
         RM_CUDA(cudaStreamSynchronize(s));
         return RMGPU_OK;
     }
-    if ((rc = host_events(2 * (size_t)nb + 1))) return rc;
-    // Any early return below leaves copies queued on `up` / `down` that still use a.p / b.p: this
-    // guard (destroyed before the DevBufs) waits for both copy streams first, so the buffers are
-    // never handed back to the pool while a copy can still touch them.
-    struct Drain {
-        bool armed = true;
-        ~Drain() {
-            if (armed) {
-                cudaStreamSynchronize(t_ctx.up);
-                cudaStreamSynchronize(t_ctx.down);
-            }
+    auto direct = [&]() -> int {
+        int r = enqueue_host_pipeline(hsrc, sp, hdst, dp, W, H, wx, wy, op, border, bval, elem, algo_h, algo_v, pitch,
+                                      R, nb, halo, s);
+        // on an error, wait for everything queued (copies may still use the freed buffers' memory)
+        cudaError_t e1 = cudaStreamSynchronize(t_ctx.up), e2 = cudaStreamSynchronize(t_ctx.down);
+        cudaError_t e3 = cudaStreamSynchronize(s);
+        if (r) return r;
+        if (e1 != cudaSuccess) return cuda_fail(e1, "host pipeline (uploads)");
+        if (e2 != cudaSuccess) return cuda_fail(e2, "host pipeline (downloads)");
+        if (e3 != cudaSuccess) return cuda_fail(e3, "host pipeline");
+        return RMGPU_OK;
+    };
+    if (!graphs) return direct();
+    // graphs only for page-locked host buffers (memcpy nodes from pageable memory are not async)
+    for (const void* hp : {hsrc, static_cast<const void*>(hdst)}) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, hp) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+            cudaGetLastError();
+            return direct();
         }
-    } drain;
-    cudaEvent_t* ev_in = t_ctx.events.data();
-    cudaEvent_t* ev_out = ev_in + nb;
-    cudaEvent_t ev_start = ev_in[2 * nb];
-    // the scratch allocations are stream-ordered on `s`: the copy streams start after them
-    RM_CUDA(cudaEventRecord(ev_start, s));
-    RM_CUDA(cudaStreamWaitEvent(t_ctx.up, ev_start, 0));
-    // contiguous host rows (pitch == row bytes == device pitch) go as plain 1-D copies
-    const bool flat_in = sp == rb && pitch == rb, flat_out = dp == rb && pitch == rb;
-    for (int k = 0; k < nb; ++k) {
-        const int r0 = k * R, n = std::min(R, H - r0);
-        char* d = static_cast<char*>(a.p) + (size_t)r0 * pitch;
-        const char* h = static_cast<const char*>(hsrc) + (size_t)r0 * sp;
-        if (flat_in) RM_CUDA(cudaMemcpyAsync(d, h, rb * n, cudaMemcpyHostToDevice, t_ctx.up));
-        else RM_CUDA(cudaMemcpy2DAsync(d, pitch, h, sp, rb, n, cudaMemcpyHostToDevice, t_ctx.up));
-        RM_CUDA(cudaEventRecord(ev_in[k], t_ctx.up));
     }
-    for (int k = 0; k < nb; ++k) {
-        const int r0 = k * R, n = std::min(R, H - r0);
-        RM_CUDA(cudaStreamWaitEvent(s, ev_in[std::min(k + 1, nb - 1)], 0));  // band k and its halo
-        const int above = std::min(halo, r0), below = std::min(halo, H - r0 - n);
-        rc = run_morph(static_cast<char*>(a.p) + (size_t)r0 * pitch, pitch, 0,
-                       static_cast<char*>(b.p) + (size_t)r0 * pitch, pitch, 0, 1, W, n, above, below, wx, wy, op,
-                       border, bval, elem, s, algo_h, algo_v);
-        if (rc) return rc;
-        RM_CUDA(cudaEventRecord(ev_out[k], s));
-        RM_CUDA(cudaStreamWaitEvent(t_ctx.down, ev_out[k], 0));
-        char* h = static_cast<char*>(hdst) + (size_t)r0 * dp;
-        const char* d = static_cast<const char*>(b.p) + (size_t)r0 * pitch;
-        if (flat_out) RM_CUDA(cudaMemcpyAsync(h, d, rb * n, cudaMemcpyDeviceToHost, t_ctx.down));
-        else RM_CUDA(cudaMemcpy2DAsync(h, dp, d, pitch, rb, n, cudaMemcpyDeviceToHost, t_ctx.down));
+    HostGraphKey key{};
+    memset(&key, 0, sizeof key);
+    key.hsrc = hsrc; key.hdst = hdst; key.sp = sp; key.dp = dp; key.W = W; key.H = H; key.wx = wx; key.wy = wy;
+    key.op = op; key.border = border; key.elem = elem; key.algo_h = algo_h; key.algo_v = algo_v; key.nb = nb;
+    key.bval = bval;
+    RM_CUDA(cudaGetDevice(&key.dev));
+    for (auto& g : t_graphs)
+        if (g.key == key) {
+            if (!g.exec) return direct();
+            RM_CUDA(cudaGraphLaunch(g.exec, s));
+            RM_CUDA(cudaStreamSynchronize(s));
+            return RMGPU_OK;
+        }
+    // capture this call's pipeline once; a call that cannot be captured runs directly from now on
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (ce == cudaSuccess) {
+        rc = enqueue_host_pipeline(hsrc, sp, hdst, dp, W, H, wx, wy, op, border, bval, elem, algo_h, algo_v, pitch, R,
+                                   nb, halo, s);
+        cudaGraph_t graph = nullptr;
+        ce = cudaStreamEndCapture(s, &graph);
+        if (rc == RMGPU_OK && ce == cudaSuccess && graph) ce = cudaGraphInstantiate(&exec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        if (rc != RMGPU_OK || ce != cudaSuccess) exec = nullptr;
     }
-    RM_CUDA(cudaStreamSynchronize(t_ctx.down));
+    cudaGetLastError();  // a failed capture leaves a sticky-free error behind
+    if (t_graphs.size() >= 8) {
+        if (t_graphs.front().exec) cudaGraphExecDestroy(t_graphs.front().exec);
+        t_graphs.erase(t_graphs.begin());
+    }
+    t_graphs.push_back({key, exec});
+    if (!exec) return direct();
+    RM_CUDA(cudaGraphLaunch(exec, s));
     RM_CUDA(cudaStreamSynchronize(s));
-    drain.armed = false;  // the buffers are freed on `s` (DevBuf): every copy that used them has completed
     return RMGPU_OK;
 }
 
