@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -580,8 +581,9 @@ struct DevBuf {
 // the two copy directions overlap each other and the kernels. The scratch images are allocated and
 // freed on `s`.
 int enqueue_host_pipeline(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int wx, int wy,
-                          int op, int border, unsigned bval, int elem, int algo_h, int algo_v, size_t pitch, int R,
-                          int nb, int halo, cudaStream_t s) {
+                          int op, int border, unsigned bval, int elem, int algo_h, int algo_v, size_t pitch,
+                          const std::vector<int>& starts, int halo, cudaStream_t s) {
+    const int nb = (int)starts.size() - 1;
     int rc;
     const size_t rb = (size_t)W * elem;
     if ((rc = host_events(3 * (size_t)nb + 2))) return rc;
@@ -603,14 +605,14 @@ int enqueue_host_pipeline(const void* hsrc, size_t sp, void* hdst, size_t dp, in
                        : cudaMemcpy2DAsync(d, pitch, h, sp, rb, n, cudaMemcpyHostToDevice, t_ctx.up);
     };
     for (int k = 0; k < nb; ++k) {
-        const int r0 = k * R, n = std::min(R, H - r0), head = std::min(n, halo);
+        const int r0 = starts[k], n = starts[k + 1] - r0, head = std::min(n, halo);
         if (head > 0 && head < n) RM_CUDA(upload(r0, head));
         RM_CUDA(cudaEventRecord(ev_head[k], t_ctx.up));
         RM_CUDA(upload(r0 + (head < n ? head : 0), head < n ? n - head : n));
         RM_CUDA(cudaEventRecord(ev_band[k], t_ctx.up));
     }
     for (int k = 0; rc == RMGPU_OK && k < nb; ++k) {
-        const int r0 = k * R, n = std::min(R, H - r0);
+        const int r0 = starts[k], n = starts[k + 1] - r0;
         RM_CUDA(cudaStreamWaitEvent(s, ev_band[k], 0));
         if (k + 1 < nb) RM_CUDA(cudaStreamWaitEvent(s, ev_head[k + 1], 0));  // halo rows below
         const int above = std::min(halo, r0), below = std::min(halo, H - r0 - n);
@@ -675,6 +677,24 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     const int nb_target = rmgpu::tune("host_bands", big ? 3 : 1);
     const int R = std::max({halo, 64, (H + nb_target - 1) / std::max(1, nb_target)});
     const int nb = (H + R - 1) / R;
+    // band rows: the first and last bands half as tall as the others (weights 1, 2, ..., 2, 1), so
+    // the pipeline's fill (first band up before any kernel) and drain (last band down after the
+    // last kernel) shrink without adding copies
+    std::vector<int> starts(1, 0);
+    if (nb >= 3 && rmgpu::tune("host_taper", 1)) {
+        const double unit = (double)H / (2.0 * nb - 2.0);
+        for (int k = 1; k < nb; ++k) starts.push_back((int)std::lround(unit * (2.0 * k - 1.0)));
+    } else {
+        for (int k = 1; k < nb; ++k) starts.push_back(std::min(H, k * R));
+    }
+    starts.push_back(H);
+    for (int k = 1; k <= nb; ++k)  // every band at least one halo (and 16 rows) tall
+        if (starts[k] - starts[k - 1] < std::max(halo, 16)) {
+            starts.assign(1, 0);
+            for (int m = 1; m < nb; ++m) starts.push_back(std::min(H, m * R));
+            starts.push_back(H);
+            break;
+        }
     if (nb < 2) {
         DevBuf a, b;
         a.s = b.s = s;
@@ -691,7 +711,7 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     }
     auto direct = [&]() -> int {
         int r = enqueue_host_pipeline(hsrc, sp, hdst, dp, W, H, wx, wy, op, border, bval, elem, algo_h, algo_v, pitch,
-                                      R, nb, halo, s);
+                                      starts, halo, s);
         // on an error, wait for everything queued (copies may still use the freed buffers' memory)
         cudaError_t e1 = cudaStreamSynchronize(t_ctx.up), e2 = cudaStreamSynchronize(t_ctx.down);
         cudaError_t e3 = cudaStreamSynchronize(s);
@@ -727,8 +747,8 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     cudaGraphExec_t exec = nullptr;
     cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
     if (ce == cudaSuccess) {
-        rc = enqueue_host_pipeline(hsrc, sp, hdst, dp, W, H, wx, wy, op, border, bval, elem, algo_h, algo_v, pitch, R,
-                                   nb, halo, s);
+        rc = enqueue_host_pipeline(hsrc, sp, hdst, dp, W, H, wx, wy, op, border, bval, elem, algo_h, algo_v, pitch,
+                                   starts, halo, s);
         cudaGraph_t graph = nullptr;
         ce = cudaStreamEndCapture(s, &graph);
         if (rc == RMGPU_OK && ce == cudaSuccess && graph) ce = cudaGraphInstantiate(&exec, graph, 0);
