@@ -21,6 +21,7 @@ cudaError_t launch_hh_u8_max(const SepParams&, int C, int bx, dim3 grid, cudaStr
 cudaError_t launch_hh_u16_min(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
 cudaError_t launch_hh_u16_max(const SepParams&, int C, int bx, dim3 grid, cudaStream_t s);
 
+
 namespace {
 
 constexpr int QM = 4;  // block minima kept in registers (q - 1 <= QM)
@@ -164,10 +165,15 @@ SepParams base_params(const MorphJob& j) {
     return p;
 }
 
-// One vertical pass over the job's rows: src (rows [-above, H + below) valid) -> out.
-cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl = 0, size_t sstride = 0) {
+// Plan of one vertical pass over the job's rows: src (rows [-above, H + below) valid) -> out.
+struct VPlan {
+    SepParams p;
+    int B;
+    dim3 grid;
+};
+bool plan_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl, size_t sstride, VPlan* vp) {
     int B = 0;
-    if (!choose_b(j.elem, j.gy, &B)) return cudaErrorInvalidValue;
+    if (!choose_b(j.elem, j.gy, &B)) return false;
     SepParams p = base_params(j);
     p.src = static_cast<const uint8_t*>(j.src);
     p.sp = j.sp;
@@ -201,20 +207,33 @@ cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl 
     rb = env_int("sep_rb", rb);
     rb = std::max(B, (rb + B - 1) / B * B);
     p.rb = rb;
-    const dim3 grid((unsigned)((p.nwords + VT - 1) / VT), (unsigned)((j.H + rb - 1) / rb), (unsigned)j.batch);
+    vp->p = p;
+    vp->B = B;
+    vp->grid = dim3((unsigned)((p.nwords + VT - 1) / VT), (unsigned)((j.H + rb - 1) / rb), (unsigned)j.batch);
+    return true;
+}
+
+cudaError_t run_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl = 0, size_t sstride = 0) {
+    VPlan vp;
+    if (!plan_v(j, out, op, oimg, pdl, sstride, &vp)) return cudaErrorInvalidValue;
     MorphJob jo = j;  // the output side of the tensor maps
     jo.dst = out;
     jo.dp = op;
     jo.dimg = oimg;
-    return launch_v(p, j.elem, j.mode, B, grid, j.stream, jo);
+    return launch_v(vp.p, j.elem, j.mode, vp.B, vp.grid, j.stream, jo);
 }
 
-// One horizontal pass over H rows: in -> job dst (stages = 2: this mode then the other, the two
-// horizontal passes of an opening / closing).
-cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int discard, int stages = 1,
-                  size_t dsstride = 0) {
+// Plan of one horizontal pass over H rows: in -> job dst (stages = 2: this mode then the other, the
+// two horizontal passes of an opening / closing).
+struct HPlan {
+    SepParams p;
+    int C, bx;
+    dim3 grid;
+};
+bool plan_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int discard, int stages, size_t dsstride,
+            HPlan* hp) {
     int C = 0;
-    if (!choose_c(j.elem, j.gx, &C)) return cudaErrorInvalidValue;
+    if (!choose_c(j.elem, j.gx, &C)) return false;
     SepParams p = base_params(j);
     p.src = static_cast<const uint8_t*>(in);
     p.sp = ip;
@@ -229,7 +248,7 @@ cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int
     // parts: ~24 resident warps per SM, each part a whole number of segments
     const int A = stages * (j.gx / C + (j.gx % C ? 1 : 0));
     const int OS = (32 - 2 * A) * C;
-    if (OS <= 0) return cudaErrorInvalidValue;
+    if (OS <= 0) return false;
     const int nseg = (j.W + OS - 1) / OS;
     const long long rowsw = (long long)p.groups * j.batch;
     // each warp keeps one segment in flight: parts of <= 8 segments (measured: 4096^2 u8 63x1 best
@@ -240,13 +259,24 @@ cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int
     p.pw = segs_per * OS;
     p.parts = (nseg + segs_per - 1) / segs_per;
     const long long warps = rowsw * p.parts;
-    const dim3 grid((unsigned)((warps + HT / 32 - 1) / (HT / 32)));
+    hp->p = p;
+    hp->C = C;
+    hp->bx = bx_code(p.g, C);
+    hp->grid = dim3((unsigned)((warps + HT / 32 - 1) / (HT / 32)));
+    return true;
+}
+
+cudaError_t run_h(const MorphJob& j, const void* in, size_t ip, size_t iimg, int discard, int stages = 1,
+                  size_t dsstride = 0) {
+    HPlan hp;
+    if (!plan_h(j, in, ip, iimg, discard, stages, dsstride, &hp)) return cudaErrorInvalidValue;
+    const SepParams& p = hp.p;
+    const int C = hp.C, bx = hp.bx;
     if (stages == 2) {
-        const int bx = bx_code(p.g, C);
-        if (j.elem == 1) return j.mode == MODE_MIN ? launch_hh_u8_min(p, C, bx, grid, j.stream) : launch_hh_u8_max(p, C, bx, grid, j.stream);
-        return j.mode == MODE_MIN ? launch_hh_u16_min(p, C, bx, grid, j.stream) : launch_hh_u16_max(p, C, bx, grid, j.stream);
+        if (j.elem == 1) return j.mode == MODE_MIN ? launch_hh_u8_min(p, C, bx, hp.grid, j.stream) : launch_hh_u8_max(p, C, bx, hp.grid, j.stream);
+        return j.mode == MODE_MIN ? launch_hh_u16_min(p, C, bx, hp.grid, j.stream) : launch_hh_u16_max(p, C, bx, hp.grid, j.stream);
     }
-    return launch_h(p, j.elem, j.mode, C, grid, j.stream);
+    return launch_h(p, j.elem, j.mode, C, hp.grid, j.stream);
 }
 
 }  // namespace

@@ -120,7 +120,12 @@ struct VW;
 template <>
 struct VW<uint8_t> {
     using Raw = uint32_t;
-    static __device__ __forceinline__ Raw load(const uint8_t* p) { return __ldg(reinterpret_cast<const unsigned int*>(p)); }
+    // COH: the rows were written earlier in this launch by another warp (chain kernel): an ordinary
+    // load, not the non-coherent path
+    template <bool COH = false>
+    static __device__ __forceinline__ Raw load(const uint8_t* p) {
+        return COH ? *reinterpret_cast<const unsigned int*>(p) : __ldg(reinterpret_cast<const unsigned int*>(p));
+    }
     static __device__ __forceinline__ uint2 unpack(Raw r) { return make_uint2(r, r << 8); }
     static __device__ __forceinline__ Raw splat(uint32_t b) { return b * 0x01010101u; }
     static __device__ __forceinline__ Raw sel(bool c, Raw a, Raw b) { return c ? a : b; }
@@ -128,7 +133,10 @@ struct VW<uint8_t> {
 template <>
 struct VW<uint16_t> {
     using Raw = uint2;
-    static __device__ __forceinline__ Raw load(const uint8_t* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+    template <bool COH = false>
+    static __device__ __forceinline__ Raw load(const uint8_t* p) {
+        return COH ? *reinterpret_cast<const uint2*>(p) : __ldg(reinterpret_cast<const uint2*>(p));
+    }
     static __device__ __forceinline__ uint2 unpack(Raw r) { return r; }
     static __device__ __forceinline__ Raw splat(uint32_t b) { return make_uint2(b * 0x00010001u, b * 0x00010001u); }
     static __device__ __forceinline__ Raw sel(bool c, Raw a, Raw b) { return make_uint2(c ? a.x : b.x, c ? a.y : b.y); }
@@ -143,117 +151,140 @@ __device__ __forceinline__ void store_partial(uint8_t* p, uint2 v, int n) {
 
 constexpr int VRMAX = 4;  // tail rows r = 2g mod B folded from re-read rows (planner keeps r <= 4)
 
+// G op= the n most recent whole-block minima M[0..n) (n warp-uniform, <= 4): one branch instead of
+// a select per register.
+template <int MODE, int QM>
+__device__ __forceinline__ uint2 fold_minima(uint2 G, const uint2 (&M)[QM], int n) {
+    static_assert(QM >= 4, "block minima");
+    switch (n) {
+    case 4: return op3<MODE>(op3<MODE>(G, M[0], M[1]), M[2], M[3]);
+    case 3: return op3<MODE>(op2<MODE>(G, M[0]), M[1], M[2]);
+    case 2: return op3<MODE>(G, M[0], M[1]);
+    case 1: return op2<MODE>(G, M[0]);
+    default: return G;
+    }
+}
+
+// The reductions of one block of B (even) output rows in 2 three-input min / max per row and
+// 16-bit-lane word (VIMNMX3 issues at the rate of the two-input form): rows are folded in pairs,
+//   T2[j] = G u trailing rows 2j .. B-1       = op3(T2[j+1], xt[2j], xt[2j+1]),   T2[B/2] = G
+//   P2[j] = leading rows 0 .. 2j+1            = op3(P2[j-1], xl[2j], xl[2j+1])
+//   out[2j]   = op3(T2[j], P2[j-1], xl[2j]),   out[2j+1] = op3(xt[2j+1], T2[j+1], P2[j])
+// with G = the r tail rows and the q-1 whole-block minima. XT / XR / XL return unpacked rows.
+template <typename T, int MODE, int B, int QM, typename XT, typename XR, typename XL, typename ST>
+__device__ __forceinline__ void vblock_reduce(int q, int r, uint2 (&M)[QM], XT xt, XR xr, XL xl, ST st) {
+    static_assert(B % 2 == 0, "rows are folded in pairs");
+    constexpr int HB = B / 2;
+    uint2 G = ident2<MODE>();
+    switch (r) {  // warp-uniform
+    case 4: G = op3<MODE>(op3<MODE>(G, xr(0), xr(1)), xr(2), xr(3)); break;
+    case 3: G = op3<MODE>(xr(0), xr(1), xr(2)); break;
+    case 2: G = op2<MODE>(xr(0), xr(1)); break;
+    case 1: G = xr(0); break;
+    default: break;
+    }
+    G = fold_minima<MODE, QM>(G, M, q - 1);
+    uint2 T2[HB + 1];
+    T2[HB] = G;
+#pragma unroll
+    for (int j = HB - 1; j >= 0; --j) T2[j] = op3<MODE>(T2[j + 1], xt(2 * j), xt(2 * j + 1));
+    uint2 P2 = xl(0);
+    st(0, op2<MODE>(T2[0], P2));
+    P2 = op2<MODE>(P2, xl(1));
+    st(1, op3<MODE>(xt(1), T2[1], P2));
+#pragma unroll
+    for (int j = 1; j < HB; ++j) {
+        const uint2 xe = xl(2 * j), xo = xl(2 * j + 1);
+        st(2 * j, op3<MODE>(T2[j], P2, xe));
+        P2 = op3<MODE>(P2, xe, xo);
+        st(2 * j + 1, op3<MODE>(xt(2 * j + 1), T2[j + 1], P2));
+    }
+#pragma unroll
+    for (int k = QM - 1; k > 0; --k) M[k] = M[k - 1];
+    M[0] = P2;
+}
+
+// B rows of one column word starting at row0 (border-aware on edge bands).
+template <typename T, int B, bool EDGE, int SPC, bool COH>
+__device__ __forceinline__ void vload_rows(const SepParams& p, const uint8_t* s, int row0,
+                                           typename VW<T>::Raw (&x)[B]) {
+    using V = VW<T>;
+    using Raw = typename V::Raw;
+    const ptrdiff_t sp = SPC ? (ptrdiff_t)SPC : (ptrdiff_t)p.sp;
+    if constexpr (EDGE) {  // border-aware (edge bands): clamp, then substitute the constant
+        const Raw CW = V::splat(p.bval);
+#pragma unroll
+        for (int m = 0; m < B; ++m) {
+            const int i = row0 + m;
+            const int ic = min(max(i, p.row_lo), p.row_hi - 1);
+            const Raw v = V::template load<COH>(s + (ptrdiff_t)ic * sp);
+            x[m] = V::sel(p.cmode && ic != i, CW, v);
+        }
+    } else if constexpr (SPC != 0) {
+        const uint8_t* pl = s + (ptrdiff_t)row0 * sp;
+#pragma unroll
+        for (int m = 0; m < B; ++m) x[m] = V::template load<COH>(pl + m * SPC);  // immediate offsets
+    } else {
+        const uint8_t* pl = s + (ptrdiff_t)row0 * sp;
+#pragma unroll
+        for (int m = 0; m < B; ++m)  // base + m * pitch: one 64-bit multiply-add (FMA pipe) per row
+            x[m] = V::template load<COH>(pl + (size_t)(uint32_t)m * (size_t)(uint32_t)sp);
+    }
+}
+
 // One block of B output rows. Window of output m (leading input row base+m):
 //   rows [base+m-2g, base+m] = T[m] u G u P[m] with
 //   T[m] = suffix of the trailing batch [base-2g, base-2g+B) from m,
 //   G    = the r rows [base-2g+B, base-(q-1)B) u whole blocks L-q+1 .. L-1 (minima M[0..q-2]),
 //   P[m] = prefix of the leading block [base, base+m].
-// All 2B (+r) loads are issued before the first reduction (no branches between them).
 // SPC: compile-time source row pitch (0 = runtime p.sp). With SPC every row of a block is a
 // compile-time offset from one base register (the strip-major intermediate of the H-first order).
-template <typename T, int MODE, int B, int QM, bool EDGE, bool FULL, int SPC>
+// All 2B (+r) loads of a block are issued before its first reduction. (Measured: loading the next
+// block's leading rows one block ahead -- B more live registers -- is slower: 4096^2 1x31 11.8 vs
+// 10.1 us, 63x63 19.8 vs 18.8 us.)
+template <typename T, int MODE, int B, int QM, bool EDGE, bool FULL, int SPC, bool COH = false>
 __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uint8_t* drow, int base, int nst,
                                        int nvalid, uint2 (&M)[QM]) {
     using V = VW<T>;
     using Raw = typename V::Raw;
     const int w1 = 2 * p.g, q = p.q, r = p.r;
-    const uint2 ID = ident2<MODE>();
-    const Raw CW = V::splat(p.bval);
     const ptrdiff_t sp = SPC ? (ptrdiff_t)SPC : (ptrdiff_t)p.sp;
-    auto ldE = [&](int i) -> Raw {  // border-aware (edge bands): clamp, then substitute the constant
-        const int ic = min(max(i, p.row_lo), p.row_hi - 1);
-        const Raw v = V::load(s + (ptrdiff_t)ic * sp);
-        return V::sel(p.cmode && ic != i, CW, v);
-    };
-    Raw xt[B], xl[B], xr[VRMAX];
-    const int tb = base - w1;                    // first trailing row
-    const int rb0 = base - (q - 1) * B - r;      // first of the r tail rows
-    auto load_lead = [&]() {
-        if constexpr (EDGE) {
-#pragma unroll
-            for (int m = 0; m < B; ++m) xl[m] = ldE(base + m);
-        } else if constexpr (SPC != 0) {
-            const uint8_t* pl = s + (ptrdiff_t)base * sp;
-#pragma unroll
-            for (int m = 0; m < B; ++m) xl[m] = V::load(pl + m * SPC);  // immediate offsets
-        } else {
-            const uint8_t* pl = s + (ptrdiff_t)base * sp;
-#pragma unroll
-            for (int m = 0; m < B; ++m) {  // pointer bumps: one 64-bit add per row
-                xl[m] = V::load(pl);
-                pl += sp;
-            }
-        }
-    };
+    Raw xt[B], xr[VRMAX], xl[B];
+    const int tb = base - w1;  // first trailing row; the r tail rows follow the batch directly
+    vload_rows<T, B, EDGE, SPC, COH>(p, s, tb, xt);
     if constexpr (EDGE) {
-#pragma unroll
-        for (int m = 0; m < B; ++m) xt[m] = ldE(tb + m);
+        const Raw CW = V::splat(p.bval);
 #pragma unroll
         for (int t = 0; t < VRMAX; ++t)
-            if (t < r) xr[t] = ldE(rb0 + t);
+            if (t < r) {
+                const int i = tb + B + t;
+                const int ic = min(max(i, p.row_lo), p.row_hi - 1);
+                xr[t] = V::sel(p.cmode && ic != i, CW, V::template load<COH>(s + (ptrdiff_t)ic * sp));
+            }
     } else {
-        const uint8_t* pt = s + (ptrdiff_t)tb * sp;
-        if constexpr (SPC != 0) {
+        const uint8_t* pt = s + (ptrdiff_t)(tb + B) * sp;
 #pragma unroll
-            for (int m = 0; m < B; ++m) xt[m] = V::load(pt + m * SPC);
-            // the r tail rows follow the trailing batch directly (rb0 = tb + B)
-#pragma unroll
-            for (int t = 0; t < VRMAX; ++t)
-                if (t < r) xr[t] = V::load(pt + (B + t) * SPC);
-        } else {
-#pragma unroll
-            for (int m = 0; m < B; ++m) {
-                xt[m] = V::load(pt);
-                pt += sp;
+        for (int t = 0; t < VRMAX; ++t)
+            if (t < r) xr[t] = V::template load<COH>(pt + (size_t)(uint32_t)t * (size_t)(uint32_t)sp);
+    }
+    vload_rows<T, B, EDGE, SPC, COH>(p, s, base, xl);
+    vblock_reduce<T, MODE, B, QM>(
+        q, r, M, [&](int m) { return V::unpack(xt[m]); }, [&](int t) { return V::unpack(xr[t]); },
+        [&](int m) { return V::unpack(xl[m]); },
+        [&](int m, uint2 o) {
+            // row m of the block: base + m * pitch as one 64-bit multiply-add (FMA pipe), not a
+            // chain of 64-bit adds on the ALU pipe the min / max instructions saturate
+            uint8_t* d = drow + (size_t)(uint32_t)m * (size_t)(uint32_t)p.dp;
+            if constexpr (FULL) {
+                W4<T>::store(d, o);
+            } else if (m < nst) {
+                if (nvalid == 4) W4<T>::store(d, o);
+                else store_partial<T>(d, o, nvalid);
             }
-            // the r tail rows follow the trailing batch directly (rb0 = tb + B)
-#pragma unroll
-            for (int t = 0; t < VRMAX; ++t) {
-                if (t < r) xr[t] = V::load(pt);
-                pt += sp;
-            }
-        }
-    }
-#ifndef SEP_VSPLIT
-    load_lead();  // all 2B (+r) loads in flight before the first reduction
-#endif
-    uint2 Tm[B];
-    uint2 acc = V::unpack(xt[B - 1]);
-    Tm[B - 1] = acc;
-#pragma unroll
-    for (int m = B - 2; m >= 0; --m) {
-        acc = op2<MODE>(acc, V::unpack(xt[m]));
-        Tm[m] = acc;
-    }
-    uint2 G = ID;
-#pragma unroll
-    for (int t = 0; t < VRMAX; ++t) G = op2<MODE>(G, t < r ? V::unpack(xr[t]) : ID);
-#pragma unroll
-    for (int k = 0; k + 1 < QM; k += 2) G = op3<MODE>(G, k < q - 1 ? M[k] : ID, k + 1 < q - 1 ? M[k + 1] : ID);
-#ifdef SEP_VSPLIT
-    asm volatile("" ::: "memory");  // leading loads after the trailing suffix: B fewer live registers
-    load_lead();
-#endif
-    uint2 P = ID;
-    uint8_t* d = drow;
-#pragma unroll
-    for (int m = 0; m < B; ++m) {
-        P = op2<MODE>(P, V::unpack(xl[m]));
-        const uint2 o = op3<MODE>(Tm[m], G, P);
-        if constexpr (FULL) {
-            W4<T>::store(d, o);
-        } else if (m < nst) {
-            if (nvalid == 4) W4<T>::store(d, o);
-            else store_partial<T>(d, o, nvalid);
-        }
-        d += p.dp;
-    }
-#pragma unroll
-    for (int k = QM - 1; k > 0; --k) M[k] = M[k - 1];
-    M[0] = P;
+        });
 }
 
-template <typename T, int MODE, int B, int QM, bool EDGE, int SPC = 0>
+template <typename T, int MODE, int B, int QM, bool EDGE, int SPC = 0, bool COH = false>
 __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s, uint8_t* d, int y0, int y1,
                                            int nvalid) {
     using V = VW<T>;
@@ -265,35 +296,22 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
     for (int k = 0; k < QM; ++k) M[k] = ID;
     // warm-up: minima of the q-1 whole blocks before block 0
     for (int L = -(p.q - 1); L < 0; ++L) {
-        const int base = i0 + L * B;
-        typename V::Raw x[B];
-        const uint8_t* pw = s + (ptrdiff_t)base * sp;
+        typename V::Raw xl[B];
+        vload_rows<T, B, EDGE, SPC, COH>(p, s, i0 + L * B, xl);
+        uint2 P = op2<MODE>(V::unpack(xl[0]), V::unpack(xl[1]));
 #pragma unroll
-        for (int m = 0; m < B; ++m) {
-            if constexpr (EDGE) {
-                const int i = base + m;
-                const int ic = min(max(i, p.row_lo), p.row_hi - 1);
-                x[m] = V::sel(p.cmode && ic != i, V::splat(p.bval), V::load(s + (ptrdiff_t)ic * sp));
-            } else if constexpr (SPC != 0) {
-                x[m] = V::load(pw + m * SPC);
-            } else {
-                x[m] = V::load(pw);
-                pw += sp;
-            }
-        }
-        uint2 P = V::unpack(x[0]);
-#pragma unroll
-        for (int m = 1; m < B; ++m) P = op2<MODE>(P, V::unpack(x[m]));
+        for (int m = 2; m + 1 < B; m += 2) P = op3<MODE>(P, V::unpack(xl[m]), V::unpack(xl[m + 1]));
 #pragma unroll
         for (int k = QM - 1; k > 0; --k) M[k] = M[k - 1];
         M[0] = P;
     }
+    (void)sp;
     for (int yb = y0; yb < y1; yb += B) {
         const int base = i0 + (yb - y0);
         uint8_t* drow = d + (ptrdiff_t)yb * (ptrdiff_t)p.dp;
         const int nst = y1 - yb;
-        if (nst >= B && nvalid == 4) vblock<T, MODE, B, QM, EDGE, true, SPC>(p, s, drow, base, nst, nvalid, M);
-        else vblock<T, MODE, B, QM, EDGE, false, SPC>(p, s, drow, base, nst, nvalid, M);
+        if (nst >= B && nvalid == 4) vblock<T, MODE, B, QM, EDGE, true, SPC, COH>(p, s, drow, base, nst, nvalid, M);
+        else vblock<T, MODE, B, QM, EDGE, false, SPC, COH>(p, s, drow, base, nst, nvalid, M);
     }
 }
 
@@ -447,20 +465,6 @@ __global__ void __launch_bounds__(VT) vtma_kernel(const SepParams p, const __gri
         const unsigned char* ts = tsb + lo;
         if (edge) fill(tsb, i0 + L * B - w1, TB);
         else mbar_wait(&ft[tslot], (uint32_t)tpar);
-        uint2 Tm[B];
-        uint2 acc = V::unpack(*reinterpret_cast<const Raw*>(ts + (B - 1) * SB));
-        Tm[B - 1] = acc;
-#pragma unroll
-        for (int m = B - 2; m >= 0; --m) {
-            acc = op2<MODE>(acc, V::unpack(*reinterpret_cast<const Raw*>(ts + m * SB)));
-            Tm[m] = acc;
-        }
-        uint2 G = ID;
-#pragma unroll
-        for (int t = 0; t < VRMAX; ++t)
-            G = op2<MODE>(G, t < r ? V::unpack(*reinterpret_cast<const Raw*>(ts + (B + t) * SB)) : ID);
-#pragma unroll
-        for (int k = 0; k + 1 < QM; k += 2) G = op3<MODE>(G, k < q - 1 ? M[k] : ID, k + 1 < q - 1 ? M[k + 1] : ID);
         // output tile L & 1: its previous TMA store (block L-2) must have finished reading it
         unsigned char* obb = outb + (size_t)(L & 1) * B * SB;
         unsigned char* ob = obb + lo;
@@ -468,15 +472,11 @@ __global__ void __launch_bounds__(VT) vtma_kernel(const SepParams p, const __gri
             if (lane == 0) bulk_wait_read1();
             __syncwarp();
         }
-        uint2 P = ID;
-#pragma unroll
-        for (int m = 0; m < B; ++m) {
-            P = op2<MODE>(P, V::unpack(*reinterpret_cast<const Raw*>(ls + m * SB)));
-            W4<T>::store(ob + m * SB, op3<MODE>(Tm[m], G, P));
-        }
-#pragma unroll
-        for (int k = QM - 1; k > 0; --k) M[k] = M[k - 1];
-        M[0] = P;
+        vblock_reduce<T, MODE, B, QM>(
+            q, r, M, [&](int m) { return V::unpack(*reinterpret_cast<const Raw*>(ts + m * SB)); },
+            [&](int t) { return V::unpack(*reinterpret_cast<const Raw*>(ts + (B + t) * SB)); },
+            [&](int m) { return V::unpack(*reinterpret_cast<const Raw*>(ls + m * SB)); },
+            [&](int m, uint2 o) { W4<T>::store(ob + m * SB, o); });
         fence_async_smem();  // the tile's generic writes before the async-proxy store reads it
         __syncwarp();
         if (lane == 0) {
@@ -500,17 +500,17 @@ struct HChunk {
     static constexpr int NW = RB / 4;        // 32-bit words per row per lane
 };
 
-template <typename T, int C>
+template <typename T, int C, bool COH = false>
 __device__ __forceinline__ void h_load_row(const uint8_t* p, uint32_t (&w)[HChunk<T, C>::NW]) {
     constexpr int NW = HChunk<T, C>::NW;
     if constexpr (NW >= 4) {  // 16 or 32 bytes
 #pragma unroll
         for (int k = 0; k < NW; k += 4) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + k / 4);
+            const uint4 v = COH ? reinterpret_cast<const uint4*>(p)[k / 4] : __ldg(reinterpret_cast<const uint4*>(p) + k / 4);
             w[k] = v.x; w[k + 1] = v.y; w[k + 2] = v.z; w[k + 3] = v.w;
         }
     } else {
-        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+        const uint2 v = COH ? *reinterpret_cast<const uint2*>(p) : __ldg(reinterpret_cast<const uint2*>(p));
         w[0] = v.x; w[1] = v.y;
     }
 }
@@ -528,7 +528,7 @@ __device__ __forceinline__ void h_store_row(uint8_t* p, const uint32_t (&w)[HChu
 // Border-aware load of one lane chunk row (chunks that reach past column 0 or W-1). Chunks start
 // at multiples of C, so a chunk is either wholly left of the image, wholly right of it, or holds
 // the last n < C real pixels followed by border pixels.
-template <typename T, int C>
+template <typename T, int C, bool COH = false>
 __device__ __forceinline__ void h_load_row_edge(const uint8_t* row, int cx, int W, int cmode, uint32_t bval,
                                                 uint32_t (&w)[HChunk<T, C>::NW]) {
     constexpr int sz = sizeof(T);
@@ -541,7 +541,7 @@ __device__ __forceinline__ void h_load_row_edge(const uint8_t* row, int cx, int 
         for (int k = 0; k < NW; ++k) w[k] = v * splat;
         return;
     }
-    h_load_row<T, C>(row + (ptrdiff_t)cx * sz, w);
+    h_load_row<T, C, COH>(row + (ptrdiff_t)cx * sz, w);
     const uint32_t rep = (cmode ? bval : (uint32_t)rp[W - 1]) * splat;
     const int nb = (W - cx) * sz;  // real bytes in the chunk (< C * sz)
 #pragma unroll
@@ -719,7 +719,7 @@ __device__ __forceinline__ void h_border_fix(uint2 (&o)[C], int X, int cx, int H
 // (compile-time). The next segment's rows are loaded before the current one is reduced.
 // STAGES = 2: the two horizontal passes of an opening (MODE = min, then max) or closing in one
 // sweep -- the first pass's result never leaves registers; halo lanes double.
-template <typename T, int MODE, int C, int BXS, int STAGES = 1>
+template <typename T, int MODE, int C, int BXS, int STAGES = 1, bool COH = false>
 __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0, size_t sp, uint8_t* drow0,
                                        int nrows, int part) {
     using HC = HChunk<T, C>;
@@ -740,15 +740,15 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
         const int cx = X + (lane - HA) * C;
         if (cx >= 0 && cx + C <= W) {
             const uint8_t* b = srow0 + (ptrdiff_t)cx * sz;
-            h_load_row<T, C>(b, q0);
-            h_load_row<T, C>(b + rs1, q1);
-            h_load_row<T, C>(b + rs2, q2);
-            h_load_row<T, C>(b + rs3, q3);
+            h_load_row<T, C, COH>(b, q0);
+            h_load_row<T, C, COH>(b + rs1, q1);
+            h_load_row<T, C, COH>(b + rs2, q2);
+            h_load_row<T, C, COH>(b + rs3, q3);
         } else {
-            h_load_row_edge<T, C>(srow0, cx, W, p.cmode, p.bval, q0);
-            h_load_row_edge<T, C>(srow0 + rs1, cx, W, p.cmode, p.bval, q1);
-            h_load_row_edge<T, C>(srow0 + rs2, cx, W, p.cmode, p.bval, q2);
-            h_load_row_edge<T, C>(srow0 + rs3, cx, W, p.cmode, p.bval, q3);
+            h_load_row_edge<T, C, COH>(srow0, cx, W, p.cmode, p.bval, q0);
+            h_load_row_edge<T, C, COH>(srow0 + rs1, cx, W, p.cmode, p.bval, q1);
+            h_load_row_edge<T, C, COH>(srow0 + rs2, cx, W, p.cmode, p.bval, q2);
+            h_load_row_edge<T, C, COH>(srow0 + rs3, cx, W, p.cmode, p.bval, q3);
         }
     };
     const int xlo = part * p.pw, xhi = min(W, xlo + p.pw);
