@@ -54,7 +54,13 @@ def parse_args(argv=None):
     p.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-threads", type=int, default=2,
+                   help="host threads issuing the step's independent plugin calls in the e2e leg (each call stays "
+                        "synchronous; two callers keep both PCIe directions busy)")
     p.add_argument("--eager", action="store_true", help="launch each op from Python instead of a CUDA graph")
+    p.add_argument("--steps-per-graph", type=int, default=0,
+                   help="steps captured into one CUDA graph (0 = as many as the rotating buffers allow and "
+                        "--steps divides into; each stream walks its share of every step, joined once per graph)")
     p.add_argument("--streams", type=int, default=2,
                    help="streams the step graph forks its independent operations over (1 = serial)")
     p.add_argument("--soak-seconds", type=float, default=1.5)
@@ -244,24 +250,36 @@ class Cfg2:
                 "l2": "no flush: 32 rotating input/output buffer pairs (1 GiB) >> 126 MB L2",
                 "parallelism": f"replicas x{self.dist.world} (independent images, no collective)"}
 
-    def e2e_setup(self):
+    def e2e_setup(self, threads=1):
+        import concurrent.futures as cf
         import torch
         self.h_in = torch.from_numpy(self.img).pin_memory()
-        self.h_out = torch.empty_like(self.h_in).pin_memory()
+        # one pinned output image per calling thread (the calls of a step are independent)
+        self.e2e_threads = max(1, threads)
+        self.h_outs = [torch.empty_like(self.h_in).pin_memory() for _ in range(self.e2e_threads)]
+        self.h_out = self.h_outs[0]
+        self.e2e_pool = cf.ThreadPoolExecutor(self.e2e_threads) if self.e2e_threads > 1 else None
 
     def e2e_step(self):
         import ctypes as C
         L = self.pkg.lib()
-        n = self.size
-        h2d = d2h = 0
-        for (wx, wy, op) in self.ops_list:
-            rc = L.rmgpu_morph_host_u8(C.c_void_p(self.h_in.data_ptr()), n, C.c_void_p(self.h_out.data_ptr()), n,
-                                       n, n, wx, wy, op, 0, 0, 0, 0)
-            if rc:
-                raise RuntimeError(f"rmgpu_morph_host_u8 failed: {rc} {L.rmgpu_last_error()}")
-            h2d += n * n
-            d2h += n * n
-        return h2d, d2h
+        h, w = self.img.shape
+
+        def run(t):  # thread t issues ops t, t + T, ...: synchronous C-ABI calls (ctypes drops the GIL)
+            out = self.h_outs[t]
+            for (wx, wy, op) in self.ops_list[t::self.e2e_threads]:
+                rc = L.rmgpu_morph_host_u8(C.c_void_p(self.h_in.data_ptr()), w, C.c_void_p(out.data_ptr()), w,
+                                           w, h, wx, wy, op, 0, 0, 0, 0)
+                if rc:
+                    raise RuntimeError(f"rmgpu_morph_host_u8 failed: {rc} {L.rmgpu_last_error()}")
+
+        if self.e2e_pool:
+            for f in [self.e2e_pool.submit(run, t) for t in range(self.e2e_threads)]:
+                f.result()
+        else:
+            run(0)
+        nb = len(self.ops_list) * h * w
+        return nb, nb
 
     def out_pixels_per_step(self):
         return len(self.ops_list) * self.size * self.size
@@ -299,17 +317,6 @@ class Cfg1(Cfg2):
         return {"workload": "cfg1: 1920x1080 u8 erode+dilate 3x3 (seed 1)", "border": "replicate",
                 "l2": "no flush: 64 rotating buffer pairs (265 MB) > L2",
                 "parallelism": f"replicas x{self.dist.world}"}
-
-    def e2e_step(self):
-        import ctypes as C
-        L = self.pkg.lib()
-        h, w = self.img.shape
-        for (wx, wy, op) in self.ops_list:
-            rc = L.rmgpu_morph_host_u8(C.c_void_p(self.h_in.data_ptr()), w, C.c_void_p(self.h_out.data_ptr()), w,
-                                       w, h, wx, wy, op, 0, 0, 0, 0)
-            if rc:
-                raise RuntimeError(rc)
-        return 2 * self.img.size, 2 * self.img.size
 
     def out_pixels_per_step(self):
         return 2 * self.img.size
@@ -731,7 +738,12 @@ def main(argv=None):
     peak, peak_src = peaks()
 
     nops = len(wl.ops)
-    ngraphs = max(1, getattr(wl, "NB", nops) // nops)
+    slots = max(1, getattr(wl, "NB", nops) // nops)  # steps the rotating buffers hold
+    spg = 1
+    if not args.eager and getattr(wl, "graphable", True):
+        want = args.steps_per_graph if args.steps_per_graph > 0 else min(slots, 32)
+        spg = max(d for d in range(1, max(1, min(want, slots, args.steps)) + 1) if args.steps % d == 0)
+    ngraphs = max(1, slots // spg)
     use_graphs = not args.eager and getattr(wl, "graphable", True)
 
     def eager_step():
@@ -769,21 +781,23 @@ def main(argv=None):
                         if i % 2:
                             share.reverse()
                         with torch.cuda.stream(lane_s):
-                            for k in share:
-                                wl.launch(wl.ops[k][1])
+                            for _ in range(spg):  # the graph's steps are independent batches too
+                                for k in share:
+                                    wl.launch(wl.ops[k][1])
                     for sd in side:
                         ev = torch.cuda.Event()
                         ev.record(sd)
                         cap.wait_event(ev)
                 else:
-                    eager_step()
+                    for _ in range(spg):
+                        eager_step()
             glaunch = pkg.launch_count() - l0
             graphs.append(g)
         for g in graphs:
             g.replay()
         torch.cuda.synchronize()
 
-    def step(i):
+    def step(i):  # spg steps per call when graphs are on
         if graphs:
             graphs[i % len(graphs)].replay()
         else:
@@ -802,12 +816,12 @@ def main(argv=None):
     torch.cuda.synchronize()
     launches0 = pkg.launch_count()
     evs[0].record(stream)
-    for i in range(args.steps):
+    for i in range(args.steps // spg):
         step(i)
     evs[1].record(stream)
     torch.cuda.synchronize()
     dist.barrier()
-    launches = pkg.launch_count() - launches0 + (glaunch * args.steps if graphs else 0)
+    launches = pkg.launch_count() - launches0 + (glaunch * (args.steps // spg) if graphs else 0)
     clocks = sampler.stop()
 
     total_ms = evs[0].elapsed_time(evs[1])
@@ -891,8 +905,13 @@ def main(argv=None):
 
     e2e = None
     if not args.no_e2e:
-        wl.e2e_setup()
+        import inspect
+        if "threads" in inspect.signature(wl.e2e_setup).parameters:
+            wl.e2e_setup(threads=args.e2e_threads)
+        else:
+            wl.e2e_setup()
         wl.e2e_step()  # warm host pool / pinned paths
+        wl.e2e_step()
         dist.barrier()
         t0 = time.perf_counter()
         h2d = d2h = 0
@@ -904,7 +923,9 @@ def main(argv=None):
         e2e = {"value": dist.world * e2e_px * args.steps / e2e_s / 1e9, "unit": "Gpixel/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": getattr(wl, "e2e_path", "C-ABI rmgpu_morph_host_u8 per op (pinned host buffers; the call "
-                                                 "pipelines H2D, kernels and D2H over row bands; synchronous)")}
+                                                 "pipelines H2D, kernels and D2H over row bands; synchronous; the "
+                                                 f"step's independent calls issued from {getattr(wl, 'e2e_threads', 1)} "
+                                                 "host thread(s))")}
 
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
@@ -916,8 +937,8 @@ def main(argv=None):
                 "vs_baseline": None, "dtype": wl.dtype,
                 "data": "synthetic (seeded counter-based generator, SURVEY.md 8d; no dataset named)",
                 "config": wl.config(),
-                "launch": (f"one CUDA graph per step ({glaunch} kernel nodes, the step's independent operations "
-                           f"forked over {args.streams} streams)") if graphs else "eager",
+                "launch": (f"CUDA graphs of {spg} step(s) ({glaunch} kernel nodes per graph, the independent "
+                           f"operations forked over {args.streams} streams, joined once per graph)") if graphs else "eager",
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                              "kernel": f"{dom}: " + ", ".join(fam_ops[dom]),

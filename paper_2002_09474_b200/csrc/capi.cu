@@ -654,6 +654,13 @@ struct HostGraphEntry {
     cudaGraphExec_t exec;  // nullptr: capture not possible for this call, run it directly
 };
 thread_local std::vector<HostGraphEntry> t_graphs;
+// host calls in flight (all threads): concurrent callers already keep both PCIe directions busy
+std::atomic<int> g_host_inflight{0};
+struct InflightGuard {
+    int n;
+    InflightGuard() : n(g_host_inflight.fetch_add(1, std::memory_order_relaxed) + 1) {}
+    ~InflightGuard() { g_host_inflight.fetch_sub(1, std::memory_order_relaxed); }
+};
 
 int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H, int wx, int wy, int op,
                int border, unsigned bval, int elem, int algo_h, int algo_v) {
@@ -674,7 +681,12 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     // shrink with more bands but every copy has a fixed cost on the copy engines: 2-4 bands with the
     // head rows uploaded separately measured best (0.52-0.56 ms per call; 6 bands 0.55-0.59,
     // 16 bands 0.72; round 1's 6 bands without the head split 0.58)
-    const int nb_target = rmgpu::tune("host_bands", big ? 3 : 1);
+    // Concurrent callers (other threads inside a host call right now): whole-image calls, the
+    // callers' uploads and downloads interleave on their own (2 threads, 4096^2 u8: 42.3 Gpix/s
+    // unbanded = 98% of the measured duplex PCIe rate, 35.6 with 3 bands each; a single caller
+    // 31.4 with 3 bands, 25.8 unbanded).
+    const InflightGuard inflight;
+    const int nb_target = rmgpu::tune("host_bands", big ? (inflight.n > 1 ? 1 : 3) : 1);
     const int R = std::max({halo, 64, (H + nb_target - 1) / std::max(1, nb_target)});
     const int nb = (H + R - 1) / R;
     // band rows: the first and last bands half as tall as the others (weights 1, 2, ..., 2, 1), so
@@ -736,8 +748,13 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     key.op = op; key.border = border; key.elem = elem; key.algo_h = algo_h; key.algo_v = algo_v; key.nb = nb;
     key.bval = bval;
     RM_CUDA(cudaGetDevice(&key.dev));
-    for (auto& g : t_graphs)
-        if (g.key == key) {
+    for (size_t gi = 0; gi < t_graphs.size(); ++gi)
+        if (t_graphs[gi].key == key) {
+            const HostGraphEntry g = t_graphs[gi];
+            if (gi + 1 != t_graphs.size()) {  // most recently used last
+                t_graphs.erase(t_graphs.begin() + (ptrdiff_t)gi);
+                t_graphs.push_back(g);
+            }
             if (!g.exec) return direct();
             RM_CUDA(cudaGraphLaunch(g.exec, s));
             RM_CUDA(cudaStreamSynchronize(s));
@@ -756,7 +773,9 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
         if (rc != RMGPU_OK || ce != cudaSuccess) exec = nullptr;
     }
     cudaGetLastError();  // a failed capture leaves a sticky-free error behind
-    if (t_graphs.size() >= 8) {
+    // least recently used out; room for a sweep of windows and ops over one pair of buffers (a
+    // cache of 8 thrashed on the 16 operations of a cfg2 step: every call captured again)
+    if (t_graphs.size() >= (size_t)std::max(1, rmgpu::tune("host_graph_cache", 64))) {
         if (t_graphs.front().exec) cudaGraphExecDestroy(t_graphs.front().exec);
         t_graphs.erase(t_graphs.begin());
     }

@@ -189,10 +189,13 @@ bool plan_v(const MorphJob& j, void* out, size_t op, size_t oimg, int pdl, size_
     p.q = 2 * j.gy / B;
     p.r = 2 * j.gy % B;
     p.nwords = (j.W + 3) / 4;
-    // bands: ~24 resident warps per SM; the warm-up (q-1 blocks per band) stays < ~50% of a band
+    // bands: one wave of the warps that are resident at this variant's register budget (u8 blocks
+    // of <= 14 rows 6 CTAs per SM, taller ones and u16 4: 63x63 at 4096^2 used to launch 824 CTAs for
+    // 592 slots); the warm-up (q-1 blocks per band) stays < ~50% of a band
     const long long cols = (long long)p.nwords * j.batch;
     const int sms = device_sm_count();
-    int bands = (int)std::max(1LL, ((long long)sms * 24 * 32 + cols - 1) / cols);
+    const int vwarps = env_int("sep_vwarps", (j.elem == 1 && B <= 14 ? 6 : 4) * (VT / 32));
+    int bands = (int)std::max(1LL, ((long long)sms * vwarps * 32 + cols - 1) / cols);
     int rb = (j.H + bands - 1) / bands;
     // the band is at least as tall as its warm-up (q-1 blocks): 4096^2 101x101 20.5 vs 21.6 us at
     // 40 rows, 63x63 flat; a 2(q-1)B floor was slower (fewer warps)
