@@ -120,12 +120,7 @@ struct VW;
 template <>
 struct VW<uint8_t> {
     using Raw = uint32_t;
-    // COH: the rows were written earlier in this launch by another warp (chain kernel): an ordinary
-    // load, not the non-coherent path
-    template <bool COH = false>
-    static __device__ __forceinline__ Raw load(const uint8_t* p) {
-        return COH ? *reinterpret_cast<const unsigned int*>(p) : __ldg(reinterpret_cast<const unsigned int*>(p));
-    }
+    static __device__ __forceinline__ Raw load(const uint8_t* p) { return __ldg(reinterpret_cast<const unsigned int*>(p)); }
     static __device__ __forceinline__ uint2 unpack(Raw r) { return make_uint2(r, r << 8); }
     static __device__ __forceinline__ Raw splat(uint32_t b) { return b * 0x01010101u; }
     static __device__ __forceinline__ Raw sel(bool c, Raw a, Raw b) { return c ? a : b; }
@@ -133,10 +128,7 @@ struct VW<uint8_t> {
 template <>
 struct VW<uint16_t> {
     using Raw = uint2;
-    template <bool COH = false>
-    static __device__ __forceinline__ Raw load(const uint8_t* p) {
-        return COH ? *reinterpret_cast<const uint2*>(p) : __ldg(reinterpret_cast<const uint2*>(p));
-    }
+    static __device__ __forceinline__ Raw load(const uint8_t* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
     static __device__ __forceinline__ uint2 unpack(Raw r) { return r; }
     static __device__ __forceinline__ Raw splat(uint32_t b) { return make_uint2(b * 0x00010001u, b * 0x00010001u); }
     static __device__ __forceinline__ Raw sel(bool c, Raw a, Raw b) { return make_uint2(c ? a.x : b.x, c ? a.y : b.y); }
@@ -205,7 +197,7 @@ __device__ __forceinline__ void vblock_reduce(int q, int r, uint2 (&M)[QM], XT x
 }
 
 // B rows of one column word starting at row0 (border-aware on edge bands).
-template <typename T, int B, bool EDGE, int SPC, bool COH>
+template <typename T, int B, bool EDGE, int SPC>
 __device__ __forceinline__ void vload_rows(const SepParams& p, const uint8_t* s, int row0,
                                            typename VW<T>::Raw (&x)[B]) {
     using V = VW<T>;
@@ -217,18 +209,18 @@ __device__ __forceinline__ void vload_rows(const SepParams& p, const uint8_t* s,
         for (int m = 0; m < B; ++m) {
             const int i = row0 + m;
             const int ic = min(max(i, p.row_lo), p.row_hi - 1);
-            const Raw v = V::template load<COH>(s + (ptrdiff_t)ic * sp);
+            const Raw v = V::load(s + (ptrdiff_t)ic * sp);
             x[m] = V::sel(p.cmode && ic != i, CW, v);
         }
     } else if constexpr (SPC != 0) {
         const uint8_t* pl = s + (ptrdiff_t)row0 * sp;
 #pragma unroll
-        for (int m = 0; m < B; ++m) x[m] = V::template load<COH>(pl + m * SPC);  // immediate offsets
+        for (int m = 0; m < B; ++m) x[m] = V::load(pl + m * SPC);  // immediate offsets
     } else {
         const uint8_t* pl = s + (ptrdiff_t)row0 * sp;
 #pragma unroll
         for (int m = 0; m < B; ++m)  // base + m * pitch: one 64-bit multiply-add (FMA pipe) per row
-            x[m] = V::template load<COH>(pl + (size_t)(uint32_t)m * (size_t)(uint32_t)sp);
+            x[m] = V::load(pl + (size_t)(uint32_t)m * (size_t)(uint32_t)sp);
     }
 }
 
@@ -242,7 +234,7 @@ __device__ __forceinline__ void vload_rows(const SepParams& p, const uint8_t* s,
 // All 2B (+r) loads of a block are issued before its first reduction. (Measured: loading the next
 // block's leading rows one block ahead -- B more live registers -- is slower: 4096^2 1x31 11.8 vs
 // 10.1 us, 63x63 19.8 vs 18.8 us.)
-template <typename T, int MODE, int B, int QM, bool EDGE, bool FULL, int SPC, bool COH = false>
+template <typename T, int MODE, int B, int QM, bool EDGE, bool FULL, int SPC>
 __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uint8_t* drow, int base, int nst,
                                        int nvalid, uint2 (&M)[QM]) {
     using V = VW<T>;
@@ -251,7 +243,7 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
     const ptrdiff_t sp = SPC ? (ptrdiff_t)SPC : (ptrdiff_t)p.sp;
     Raw xt[B], xr[VRMAX], xl[B];
     const int tb = base - w1;  // first trailing row; the r tail rows follow the batch directly
-    vload_rows<T, B, EDGE, SPC, COH>(p, s, tb, xt);
+    vload_rows<T, B, EDGE, SPC>(p, s, tb, xt);
     if constexpr (EDGE) {
         const Raw CW = V::splat(p.bval);
 #pragma unroll
@@ -259,15 +251,15 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
             if (t < r) {
                 const int i = tb + B + t;
                 const int ic = min(max(i, p.row_lo), p.row_hi - 1);
-                xr[t] = V::sel(p.cmode && ic != i, CW, V::template load<COH>(s + (ptrdiff_t)ic * sp));
+                xr[t] = V::sel(p.cmode && ic != i, CW, V::load(s + (ptrdiff_t)ic * sp));
             }
     } else {
         const uint8_t* pt = s + (ptrdiff_t)(tb + B) * sp;
 #pragma unroll
         for (int t = 0; t < VRMAX; ++t)
-            if (t < r) xr[t] = V::template load<COH>(pt + (size_t)(uint32_t)t * (size_t)(uint32_t)sp);
+            if (t < r) xr[t] = V::load(pt + (size_t)(uint32_t)t * (size_t)(uint32_t)sp);
     }
-    vload_rows<T, B, EDGE, SPC, COH>(p, s, base, xl);
+    vload_rows<T, B, EDGE, SPC>(p, s, base, xl);
     vblock_reduce<T, MODE, B, QM>(
         q, r, M, [&](int m) { return V::unpack(xt[m]); }, [&](int t) { return V::unpack(xr[t]); },
         [&](int m) { return V::unpack(xl[m]); },
@@ -284,7 +276,7 @@ __device__ __forceinline__ void vblock(const SepParams& p, const uint8_t* s, uin
         });
 }
 
-template <typename T, int MODE, int B, int QM, bool EDGE, int SPC = 0, bool COH = false>
+template <typename T, int MODE, int B, int QM, bool EDGE, int SPC = 0>
 __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s, uint8_t* d, int y0, int y1,
                                            int nvalid) {
     using V = VW<T>;
@@ -297,7 +289,7 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
     // warm-up: minima of the q-1 whole blocks before block 0
     for (int L = -(p.q - 1); L < 0; ++L) {
         typename V::Raw xl[B];
-        vload_rows<T, B, EDGE, SPC, COH>(p, s, i0 + L * B, xl);
+        vload_rows<T, B, EDGE, SPC>(p, s, i0 + L * B, xl);
         uint2 P = op2<MODE>(V::unpack(xl[0]), V::unpack(xl[1]));
 #pragma unroll
         for (int m = 2; m + 1 < B; m += 2) P = op3<MODE>(P, V::unpack(xl[m]), V::unpack(xl[m + 1]));
@@ -310,8 +302,8 @@ __device__ __forceinline__ void vpass_body(const SepParams& p, const uint8_t* s,
         const int base = i0 + (yb - y0);
         uint8_t* drow = d + (ptrdiff_t)yb * (ptrdiff_t)p.dp;
         const int nst = y1 - yb;
-        if (nst >= B && nvalid == 4) vblock<T, MODE, B, QM, EDGE, true, SPC, COH>(p, s, drow, base, nst, nvalid, M);
-        else vblock<T, MODE, B, QM, EDGE, false, SPC, COH>(p, s, drow, base, nst, nvalid, M);
+        if (nst >= B && nvalid == 4) vblock<T, MODE, B, QM, EDGE, true, SPC>(p, s, drow, base, nst, nvalid, M);
+        else vblock<T, MODE, B, QM, EDGE, false, SPC>(p, s, drow, base, nst, nvalid, M);
     }
 }
 
@@ -500,17 +492,17 @@ struct HChunk {
     static constexpr int NW = RB / 4;        // 32-bit words per row per lane
 };
 
-template <typename T, int C, bool COH = false>
+template <typename T, int C>
 __device__ __forceinline__ void h_load_row(const uint8_t* p, uint32_t (&w)[HChunk<T, C>::NW]) {
     constexpr int NW = HChunk<T, C>::NW;
     if constexpr (NW >= 4) {  // 16 or 32 bytes
 #pragma unroll
         for (int k = 0; k < NW; k += 4) {
-            const uint4 v = COH ? reinterpret_cast<const uint4*>(p)[k / 4] : __ldg(reinterpret_cast<const uint4*>(p) + k / 4);
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + k / 4);
             w[k] = v.x; w[k + 1] = v.y; w[k + 2] = v.z; w[k + 3] = v.w;
         }
     } else {
-        const uint2 v = COH ? *reinterpret_cast<const uint2*>(p) : __ldg(reinterpret_cast<const uint2*>(p));
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
         w[0] = v.x; w[1] = v.y;
     }
 }
@@ -528,7 +520,7 @@ __device__ __forceinline__ void h_store_row(uint8_t* p, const uint32_t (&w)[HChu
 // Border-aware load of one lane chunk row (chunks that reach past column 0 or W-1). Chunks start
 // at multiples of C, so a chunk is either wholly left of the image, wholly right of it, or holds
 // the last n < C real pixels followed by border pixels.
-template <typename T, int C, bool COH = false>
+template <typename T, int C>
 __device__ __forceinline__ void h_load_row_edge(const uint8_t* row, int cx, int W, int cmode, uint32_t bval,
                                                 uint32_t (&w)[HChunk<T, C>::NW]) {
     constexpr int sz = sizeof(T);
@@ -541,7 +533,7 @@ __device__ __forceinline__ void h_load_row_edge(const uint8_t* row, int cx, int 
         for (int k = 0; k < NW; ++k) w[k] = v * splat;
         return;
     }
-    h_load_row<T, C, COH>(row + (ptrdiff_t)cx * sz, w);
+    h_load_row<T, C>(row + (ptrdiff_t)cx * sz, w);
     const uint32_t rep = (cmode ? bval : (uint32_t)rp[W - 1]) * splat;
     const int nb = (W - cx) * sz;  // real bytes in the chunk (< C * sz)
 #pragma unroll
@@ -719,7 +711,7 @@ __device__ __forceinline__ void h_border_fix(uint2 (&o)[C], int X, int cx, int H
 // (compile-time). The next segment's rows are loaded before the current one is reduced.
 // STAGES = 2: the two horizontal passes of an opening (MODE = min, then max) or closing in one
 // sweep -- the first pass's result never leaves registers; halo lanes double.
-template <typename T, int MODE, int C, int BXS, int STAGES = 1, bool COH = false>
+template <typename T, int MODE, int C, int BXS, int STAGES = 1>
 __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0, size_t sp, uint8_t* drow0,
                                        int nrows, int part) {
     using HC = HChunk<T, C>;
@@ -740,15 +732,15 @@ __device__ __forceinline__ void h_item(const SepParams& p, const uint8_t* srow0,
         const int cx = X + (lane - HA) * C;
         if (cx >= 0 && cx + C <= W) {
             const uint8_t* b = srow0 + (ptrdiff_t)cx * sz;
-            h_load_row<T, C, COH>(b, q0);
-            h_load_row<T, C, COH>(b + rs1, q1);
-            h_load_row<T, C, COH>(b + rs2, q2);
-            h_load_row<T, C, COH>(b + rs3, q3);
+            h_load_row<T, C>(b, q0);
+            h_load_row<T, C>(b + rs1, q1);
+            h_load_row<T, C>(b + rs2, q2);
+            h_load_row<T, C>(b + rs3, q3);
         } else {
-            h_load_row_edge<T, C, COH>(srow0, cx, W, p.cmode, p.bval, q0);
-            h_load_row_edge<T, C, COH>(srow0 + rs1, cx, W, p.cmode, p.bval, q1);
-            h_load_row_edge<T, C, COH>(srow0 + rs2, cx, W, p.cmode, p.bval, q2);
-            h_load_row_edge<T, C, COH>(srow0 + rs3, cx, W, p.cmode, p.bval, q3);
+            h_load_row_edge<T, C>(srow0, cx, W, p.cmode, p.bval, q0);
+            h_load_row_edge<T, C>(srow0 + rs1, cx, W, p.cmode, p.bval, q1);
+            h_load_row_edge<T, C>(srow0 + rs2, cx, W, p.cmode, p.bval, q2);
+            h_load_row_edge<T, C>(srow0 + rs3, cx, W, p.cmode, p.bval, q3);
         }
     };
     const int xlo = part * p.pw, xhi = min(W, xlo + p.pw);

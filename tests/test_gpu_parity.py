@@ -450,6 +450,27 @@ def test_host_entry_pipelined_bands(gpu, restatement):
             assert np.array_equal(got, want), (dtype, wx, wy, op, border)
 
 
+def test_host_entry_concurrent_callers(gpu, restatement):
+    # several threads inside the synchronous host entry at once (ctypes drops the GIL): every call has
+    # its own streams and graph cache, the band count follows the number of calls in flight, and a
+    # sweep of more windows than the old 8-entry graph cache held still replays cached graphs
+    import concurrent.futures as cf
+    img = restatement.generate(4096, 2304, 91, dtype=np.uint8)  # >= 8 MB: pipelined when alone
+    windows = [(3, 3), (7, 7), (15, 15), (31, 31), (63, 63), (101, 101), (31, 1), (1, 31), (9, 21), (5, 5)]
+    jobs = [(wx, wy, op) for (wx, wy) in windows for op in (ERODE, DILATE)]
+    want = {j: restatement.morph(img, j[0], j[1], j[2], REPLICATE, 0) for j in jobs}
+
+    def run(j):
+        fn = gpu.erode if j[2] == ERODE else gpu.dilate
+        return j, fn(img, gpu.StructuringElement(j[0], j[1]), gpu.BorderPolicy(REPLICATE, 0))
+
+    for workers in (3, 1):
+        with cf.ThreadPoolExecutor(workers) as ex:
+            for rep in range(2):  # the second sweep replays the cached graphs
+                for j, got in ex.map(run, jobs):
+                    assert np.array_equal(got, want[j]), (workers, rep, j)
+
+
 def test_transpose_tiles(gpu, restatement):
     import torch
     for dt in (np.uint8, np.uint16, np.uint32):
