@@ -151,6 +151,13 @@ __device__ __forceinline__ uint32_t opn(const uint32_t* v) {
 // unpacking. u16: a lane owns 8 pixels = 4 u16x2 words. Both carry 2 extra words: the column
 // word(s) just left of the strip (lane 0) / right of it (lane 31).
 // ---------------------------------------------------------------------------------------------
+// x << 8 as a multiply: IMAD on the FMA pipe instead of a permute / shift on the ALU pipe
+__device__ __forceinline__ uint32_t shl8_fma(uint32_t x) {
+    uint32_t y;
+    asm("mul.lo.u32 %0, %1, 256;" : "=r"(y) : "r"(x));
+    return y;
+}
+
 template <typename T>
 struct RowW;
 template <>
@@ -181,10 +188,11 @@ struct ColCore {
             const uint32_t x = lane == 0 ? xx.y : xx.x;  // left: bytes x0-4..x0-1; right: x0+512..
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                e[k] = prmt(w[k], w[k], 0x2301);  // even pixels into the high bytes
+                e[k] = shl8_fma(w[k]);            // even pixels into the high bytes: x * 256 on the FMA
+                                                  // pipe (the min / max and permutes saturate the ALU pipe)
                 e[4 + k] = w[k];                  // odd pixels already there
             }
-            e[8] = prmt(x, x, 0x2301);
+            e[8] = shl8_fma(x);
             e[9] = x;
         } else {
 #pragma unroll

@@ -16,7 +16,7 @@ from tests.gpu_util import empty_device, to_device, to_host  # noqa: E402
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 R = oracle.restatement()
-KNOBS = [{}, {"sep_hfirst": 0}, {"sep_strip": 0}, {"sep_vbulk": 1}, {"sep_notma": 0}, {"sep_hh": 2},
+KNOBS = [{}, {"sep_vwarps": 8}, {"sep_hfirst": 0}, {"sep_strip": 0}, {"sep_vbulk": 1}, {"sep_notma": 0}, {"sep_hh": 2},
          {"sep_hh": 0}, {"sep_parts": 3}, {"sep_rb": 16}, {"sep_pdl": 1}, {"sep_c16_short": 0}]
 t0, n, bad = time.time(), 0, 0
 while time.time() - t0 < budget:
