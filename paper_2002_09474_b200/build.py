@@ -36,7 +36,7 @@ CU_SOURCES = ["capi.cu", "morph_generic.cu", "morph_stream.cu", "morph_phase.cu"
               "transpose.cu",
               "generate.cu", "morph_fuse.cu"]
 # K4 instantiations: morph_fuse_inst.cu compiled once per (pixel size, mode, block size B)
-FUSE_VARIANTS = [(sz, mx, b) for sz in (1, 2) for mx in (0, 1) for b in ((8, 12, 16, 20, 24) if sz == 1 else (8, 12, 16))]
+FUSE_VARIANTS = [(sz, mx, b) for sz in (1, 2) for mx in (0, 1) for b in ((12, 20) if sz == 1 else (8, 12))]
 HOST_SOURCES = [os.path.join("host", "rectmorph_b200.cpp"), os.path.join("host", "pgm_b200.cpp")]
 
 

@@ -14,11 +14,11 @@ namespace fuse {
 #define RM_DECL(TN, MN, BB)                                                                                  \
     cudaError_t launch_##TN##_##MN##_b##BB(const FuseParams&, int, dim3, int, cudaStream_t, const CUtensorMap&, \
                                         const CUtensorMap&);
-#define RM_DECL_B(TN, MN) RM_DECL(TN, MN, 8) RM_DECL(TN, MN, 12) RM_DECL(TN, MN, 16) RM_DECL(TN, MN, 20) RM_DECL(TN, MN, 24)
+#define RM_DECL_B(TN, MN) RM_DECL(TN, MN, 12) RM_DECL(TN, MN, 20)
 RM_DECL_B(u8, min)
 RM_DECL_B(u8, max)
-RM_DECL(u16, min, 8) RM_DECL(u16, min, 12) RM_DECL(u16, min, 16)
-RM_DECL(u16, max, 8) RM_DECL(u16, max, 12) RM_DECL(u16, max, 16)
+RM_DECL(u16, min, 8) RM_DECL(u16, min, 12)
+RM_DECL(u16, max, 8) RM_DECL(u16, max, 12)
 #undef RM_DECL_B
 #undef RM_DECL
 
@@ -38,7 +38,9 @@ cudaError_t launch_kernel(const void* kern, const FuseParams& p, dim3 grid, int 
 
 namespace {
 
-constexpr int kB[] = {8, 12, 16, 20, 24};
+// block sizes with instantiations (u8: 12, 20; u16: 8, 12): K4 is a knob-only path, windows whose
+// 2 gy does not split over one of them stay on K3
+constexpr int kB[] = {8, 12, 20};
 constexpr int kSmemPerSm = 228 * 1024;  // B200: shared memory per SM (1 KB reserved per CTA)
 
 struct Plan {
@@ -89,7 +91,7 @@ bool plan(const MorphJob& j, Plan* pl) {
     const int want_nt = tune("fuse_nt", FT > 256 ? 8 : 4);
     const int pair = std::min(2, std::max(1, tune("fuse_pair", 2)));
     for (int B : kB) {
-        if (j.elem == 2 && B > 16) continue;
+        if (j.elem == 2 ? B > 12 : B == 8) continue;
         if (forced_b && B != forced_b) continue;
         const int q = 2 * j.gy / B, r = 2 * j.gy % B;
         if (q < 1 || r > RMAXG || q - 1 > QM) continue;
@@ -172,15 +174,15 @@ cudaError_t dispatch(const FuseParams& fp, int mode, int B, int bxs, dim3 grid, 
     case BB: return launch_##TN##_##MN##_b##BB(fp, bxs, grid, smem, s, m, g);
     if (SZ == 1) {
         if (mode == MODE_MIN) {
-            switch (B) { RM_CASE(u8, min, 8) RM_CASE(u8, min, 12) RM_CASE(u8, min, 16) RM_CASE(u8, min, 20) RM_CASE(u8, min, 24) }
+            switch (B) { RM_CASE(u8, min, 12) RM_CASE(u8, min, 20) }
         } else {
-            switch (B) { RM_CASE(u8, max, 8) RM_CASE(u8, max, 12) RM_CASE(u8, max, 16) RM_CASE(u8, max, 20) RM_CASE(u8, max, 24) }
+            switch (B) { RM_CASE(u8, max, 12) RM_CASE(u8, max, 20) }
         }
     } else {
         if (mode == MODE_MIN) {
-            switch (B) { RM_CASE(u16, min, 8) RM_CASE(u16, min, 12) RM_CASE(u16, min, 16) }
+            switch (B) { RM_CASE(u16, min, 8) RM_CASE(u16, min, 12) }
         } else {
-            switch (B) { RM_CASE(u16, max, 8) RM_CASE(u16, max, 12) RM_CASE(u16, max, 16) }
+            switch (B) { RM_CASE(u16, max, 8) RM_CASE(u16, max, 12) }
         }
     }
 #undef RM_CASE

@@ -1,6 +1,6 @@
 // morph_fuse_inst.cu -- K4 instantiations for one (pixel size, mode, block size B), selected at
 // build time: build.py compiles this file once per variant with -DFUSE_SZ={1,2} -DFUSE_MAX={0,1}
-// -DFUSE_B={8,12,16,20,24}. Each object holds every horizontal chunk class g mod C of that B
+// -DFUSE_B={12,20} (u8) / {8,12} (u16). Each object holds every horizontal chunk class g mod C of that B
 // (+ the u8 short-wing variants 36..39, see sep::h_lane_pass).
 #include "morph_fuse.cuh"
 

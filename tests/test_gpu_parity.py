@@ -349,11 +349,29 @@ def test_sep_passes_fuzz(gpu, restatement, dtype, knobs):
     # K3 (separable streaming passes through L2) under every planner knob that changes its launch
     # geometry: every chunk class g mod C, block size / tail r, edge bands, ragged words, batches
     # and row bands, both borders
+    _planner_fuzz(gpu, restatement, dtype, knobs, dict(SEP_KNOBS[knobs]), "sep")
+
+
+FUSE_KNOBS = [
+    {"fuse": 1},                                  # K4 (single-pass fused kernel) with its defaults
+    {"fuse": 1, "fuse_pf": 1, "fuse_nt": 2},      # one block of TMA prefetch, two tile slots
+    {"fuse": 1, "fuse_pair": 1, "fuse_b": 12},    # one block per TMA box, 12-row blocks only
+]
+
+
+@pytest.mark.parametrize("knobs", range(len(FUSE_KNOBS)))
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_fused_kernel_fuzz(gpu, restatement, dtype, knobs):
+    # K4 (vertical and horizontal pass in one kernel, intermediate in shared memory; off by default)
+    # on the same random images, batches and row bands; windows it declines stay on K3
+    _planner_fuzz(gpu, restatement, dtype, 100 + knobs, dict(FUSE_KNOBS[knobs]), "fuse")
+
+
+def _planner_fuzz(gpu, restatement, dtype, knobs, knob_set, expect):
     import torch
     rng = np.random.default_rng(1234 + 7 * knobs + np.dtype(dtype).itemsize)
     mx = int(np.iinfo(dtype).max)
     es = np.dtype(dtype).itemsize
-    knob_set = dict(SEP_KNOBS[knobs])
     for k, v in knob_set.items():
         gpu.debug_set(k, v)
     try:
@@ -397,7 +415,7 @@ def test_sep_passes_fuzz(gpu, restatement, dtype, knobs):
                 want = restatement.morph(img, wx, wy, op, border, bval)
                 assert np.array_equal(got, want), ("image", knobs, c, w, h, wx, wy, op, border)
             seen.add(gpu.plan_name(es, w, h, wx, wy, op).split("_")[0])
-        assert "sep" in seen, seen
+        assert expect in seen, seen
     finally:
         for k in knob_set:
             gpu.debug_set(k, -1)
