@@ -325,7 +325,8 @@ class Cfg1(Cfg2):
 class Cfg4:
     """512 u16 1024x1024 images (seed 4, stream = image index), opening 21x21 replicate, batch sharded
     over the ranks (contiguous shards, no collective). One step = the rank's whole shard."""
-    e2e_path = "pinned host shard -> device (H2D), morph_batched_device opening, D2H, synchronised"
+    e2e_path = ("pinned host shard -> device in chunks of 64 images (H2D), morph_batched_device opening per chunk, "
+                "D2H; three streams, synchronised at the end of the step")
     name = "cfg4"
     dtype = "u16"
     graphable = False
@@ -367,11 +368,33 @@ class Cfg4:
         self.h_out = torch.empty_like(self.h_in).pin_memory()
 
     def e2e_step(self):
+        # the shard in chunks of 64 images over three streams: the upload of chunk k+1, the opening of
+        # chunk k and the download of chunk k-1 overlap (both PCIe directions busy)
         import torch
-        d_in = self.h_in.to("cuda", non_blocking=True)
-        d_out = torch.empty_like(d_in)
-        self.pkg.morph_batched_device(d_in, d_out, self.WIN, self.WIN, OPEN)
-        self.h_out.copy_(d_out, non_blocking=True)
+        if not hasattr(self, "e2e_streams"):
+            self.e2e_streams = [torch.cuda.Stream() for _ in range(3)]
+            self.e2e_din = torch.empty_like(self.src)
+            self.e2e_dout = torch.empty_like(self.src)
+        up, run, down = self.e2e_streams
+        main = torch.cuda.current_stream()
+        for st in (up, run, down):
+            st.wait_stream(main)
+        step = 64
+        for k0 in range(0, self.count, step):
+            k1 = min(self.count, k0 + step)
+            with torch.cuda.stream(up):
+                self.e2e_din[k0:k1].copy_(self.h_in[k0:k1], non_blocking=True)
+                ev_up = torch.cuda.Event()
+                ev_up.record(up)
+            with torch.cuda.stream(run):
+                run.wait_event(ev_up)
+                self.pkg.morph_batched_device(self.e2e_din[k0:k1], self.e2e_dout[k0:k1], self.WIN, self.WIN, OPEN,
+                                              stream=run)
+                ev_run = torch.cuda.Event()
+                ev_run.record(run)
+            with torch.cuda.stream(down):
+                down.wait_event(ev_run)
+                self.h_out[k0:k1].copy_(self.e2e_dout[k0:k1], non_blocking=True)
         torch.cuda.synchronize()
         nbytes = self.h_in.numel() * 2
         return nbytes, nbytes
@@ -401,7 +424,8 @@ class Cfg4:
 class Cfg5:
     """32768^2 u8 (seed 5) dilation 63x63 replicate, split into G row bands; each step exchanges the
     31-row halos with the neighbouring ranks (NCCL point-to-point) and computes the band."""
-    e2e_path = "pinned host band+halo -> device (H2D), halo exchange + morph_band, D2H, synchronised"
+    e2e_path = ("one rank: C-ABI rmgpu_morph_host_u8 on the whole pinned image (synchronous, pipelined over row "
+                "bands); several ranks: pinned host band+halo -> device (H2D), halo exchange + morph_band, D2H")
     name = "cfg5"
     dtype = "u8"
     graphable = False
@@ -472,6 +496,17 @@ class Cfg5:
 
     def e2e_step(self):
         import torch
+        if self.dist.world == 1:
+            # one rank: the band is the whole image -- the synchronous C-ABI host call (it pipelines
+            # the upload, the kernels and the download over row bands itself)
+            import ctypes as C
+            L = self.pkg.lib()
+            n = self.SIZE
+            rc = L.rmgpu_morph_host_u8(C.c_void_p(self.h_in.data_ptr()), n, C.c_void_p(self.h_out.data_ptr()), n,
+                                       n, n, self.WIN, self.WIN, DILATE, 0, 0, 0, 0)
+            if rc:
+                raise RuntimeError(f"rmgpu_morph_host_u8 failed: {rc} {L.rmgpu_last_error()}")
+            return self.h_in.numel(), self.h_out.numel()
         self.buf.copy_(self.h_in, non_blocking=True)
         self.launch(None)
         self.h_out.copy_(self.out, non_blocking=True)

@@ -654,6 +654,7 @@ struct HostGraphEntry {
     cudaGraphExec_t exec;  // nullptr: capture not possible for this call, run it directly
 };
 thread_local std::vector<HostGraphEntry> t_graphs;
+thread_local std::vector<HostGraphKey> t_seen;  // keys met once (not captured yet)
 // host calls in flight (all threads): concurrent callers already keep both PCIe directions busy
 std::atomic<int> g_host_inflight{0};
 struct InflightGuard {
@@ -686,7 +687,10 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
     // unbanded = 98% of the measured duplex PCIe rate, 35.6 with 3 bands each; a single caller
     // 31.4 with 3 bands, 25.8 unbanded).
     const InflightGuard inflight;
-    const int nb_target = rmgpu::tune("host_bands", big ? (inflight.n > 1 ? 1 : 3) : 1);
+    // Images of hundreds of MB: a band per 64 MB up to 16 (the fill and drain are one band each and
+    // the per-copy cost no longer matters: 1 GiB in 16 bands ~ 1/16 of the transfer time exposed).
+    const int by_size = (int)std::min<size_t>(16, std::max<size_t>(3, (rb * (size_t)H) >> 26));
+    const int nb_target = rmgpu::tune("host_bands", big ? (inflight.n > 1 ? 1 : by_size) : 1);
     const int R = std::max({halo, 64, (H + nb_target - 1) / std::max(1, nb_target)});
     const int nb = (H + R - 1) / R;
     // band rows: the first and last bands half as tall as the others (weights 1, 2, ..., 2, 1), so
@@ -760,7 +764,22 @@ int host_morph(const void* hsrc, size_t sp, void* hdst, size_t dp, int W, int H,
             RM_CUDA(cudaStreamSynchronize(s));
             return RMGPU_OK;
         }
-    // capture this call's pipeline once; a call that cannot be captured runs directly from now on
+    // A key seen for the first time runs directly and is only remembered: a caller that streams new
+    // buffers through (every call a new key) never pays for captures it would not replay. The second
+    // call with the same key captures the pipeline; a call that cannot be captured runs directly
+    // from then on.
+    bool seen_once = false;
+    for (size_t gi = 0; gi < t_seen.size(); ++gi)
+        if (t_seen[gi] == key) {
+            seen_once = true;
+            t_seen.erase(t_seen.begin() + (ptrdiff_t)gi);
+            break;
+        }
+    if (!seen_once) {
+        if (t_seen.size() >= 64) t_seen.erase(t_seen.begin());
+        t_seen.push_back(key);
+        return direct();
+    }
     cudaGraphExec_t exec = nullptr;
     cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
     if (ce == cudaSuccess) {
