@@ -8,10 +8,14 @@
 // order in morph_sep.cu: horizontal first on whole images and row bands):
 //
 //  * V (vertical pass): one thread per 4-pixel column word streams down a band of rows with
-//    plain coalesced loads. Block van Herk with blocks of B rows: out = min3(T[m], G, P[m]) where
-//    P is the running prefix of the leading block, T the suffix of the trailing rows (re-read: they
+//    plain coalesced loads. Block van Herk with blocks of B rows: out = T[m] u G u P[m] where
+//    P is the prefix of the leading block, T the suffix of the trailing rows (re-read: they
 //    were loaded w_y rows earlier and are still in L2) and G the r tail rows plus the minimum of
-//    the q-1 whole blocks in between (block minima kept in registers). Reading the strip-major
+//    the q-1 whole blocks in between (block minima kept in registers). The rows are folded in
+//    pairs with three-input min / max (vblock_reduce): 2 VIMNMX3 per row and 16-bit-lane word --
+//    all min / max, byte permutes, selects and shifts share the ALU pipe (one warp instruction
+//    every second cycle per scheduler, tools/ubench/pipes.cu), so shifts and row addresses go to
+//    the FMA pipe (IMAD.SHL / IMAD.WIDE). Reading the strip-major
 //    intermediate (128-pixel strips) the row pitch is a compile-time constant, so every row of a
 //    block is an immediate offset from one register. Large images: the same algorithm fed by a
 //    per-warp TMA pipeline (tensor boxes or 1-D bulk copies, output by TMA store).
