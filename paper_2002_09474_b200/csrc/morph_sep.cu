@@ -334,7 +334,11 @@ cudaError_t run_compound(const MorphJob& j, void* tmp) {
     h.dst = t2;
     h.dp = tp;
     h.dimg = timg;
-    if ((e = run_h(h, t1, tp, timg, 1, 2)) != cudaSuccess) return e;
+    // the first intermediate's lines are dropped from L2 after their last read only while they can
+    // still be there unwritten (on cfg4's 1 GiB they are long written back: the discards were 3% of
+    // the sweep's instructions)
+    const int discard = env_int("sep_discard", timg * (size_t)j.batch <= ((size_t)64 << 20) ? 1 : 0);
+    if ((e = run_h(h, t1, tp, timg, discard, 2)) != cudaSuccess) return e;
     MorphJob v = j;  // second op, vertical: t2 -> dst (rows outside the image: the image border)
     v.mode = second;
     v.src = t2;
