@@ -144,6 +144,19 @@ __device__ __forceinline__ uint32_t opn(const uint32_t* v) {
     else return op3<MODE>(op3<MODE>(op3<MODE>(v[0], v[1], v[2]), v[3], v[4]), v[5], v[6]);
 }
 
+// Two windows of N (5 or 7) consecutive words whose starts are D (1 or 2) apart, a = v[0..N) and
+// b = v[D..N+D): the words both contain are reduced once and each window adds its own with one
+// three-input instruction -- N == 7: 4 instructions for both instead of 6, N == 5: 3 instead of 4.
+template <int MODE, int N, int D>
+__device__ __forceinline__ void opn_pair(const uint32_t* v, uint32_t& a, uint32_t& b) {
+    static_assert((N == 5 || N == 7) && (D == 1 || D == 2), "paired windows");
+    uint32_t c = op3<MODE>(v[2], v[3], v[4]);
+    if constexpr (N == 7) c = op3<MODE>(c, v[5], v[6]);
+    a = op3<MODE>(c, v[0], v[1]);
+    if constexpr (D == 1) b = op3<MODE>(c, v[1], v[N]);
+    else b = op3<MODE>(c, v[N], v[N + 1]);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Per-row word sets. u8: a lane owns 16 pixels = 4 raw words; min/max run on 16-bit lanes of
 // the raw word (odd pixels, in the high bytes: the high byte of a 16-bit min/max is the min/max
@@ -242,8 +255,13 @@ struct ColCore {
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t oe = opn<MODE, 2 * GX + 1>(&U[4 * k - GX + UB]);
-                const uint32_t oo = opn<MODE, 2 * GX + 1>(&U[4 * k + 1 - GX + UB]);
+                uint32_t oe, oo;  // windows of the even / odd pixel pairs: one U index apart
+                if constexpr (GX >= 2) {
+                    opn_pair<MODE, 2 * GX + 1, 1>(&U[4 * k - GX + UB], oe, oo);
+                } else {
+                    oe = opn<MODE, 2 * GX + 1>(&U[4 * k - GX + UB]);
+                    oo = opn<MODE, 2 * GX + 1>(&U[4 * k + 1 - GX + UB]);
+                }
                 o[k] = prmt(oe, oo, 0x7351);
             }
         } else {
@@ -275,8 +293,13 @@ struct ColCore {
                 const int k = (i + 4) / 2 - 2, m = (i + 4) % 2;
                 U[i + UB] = m == 0 ? Wf[k + 2] : prmt(Wf[k + 2], Wf[k + 3], 0x5432);
             }
+            if constexpr (GX >= 2) {  // neighbouring output words: windows two U indices apart
 #pragma unroll
-            for (int k = 0; k < 4; ++k) o[k] = opn<MODE, 2 * GX + 1>(&U[2 * k - GX + UB]);
+                for (int k = 0; k < 4; k += 2) opn_pair<MODE, 2 * GX + 1, 2>(&U[2 * k - GX + UB], o[k], o[k + 1]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) o[k] = opn<MODE, 2 * GX + 1>(&U[2 * k - GX + UB]);
+            }
         }
         return make_uint4(o[0], o[1], o[2], o[3]);
     }
@@ -432,44 +455,73 @@ morph_col_kernel(const ColParams p, const __grid_constant__ CUtensorMap tmap, co
             const unsigned char* rows = ring + cslot * SLOTB;
             if (edge) fix_block_columns<T, GX>(ring + cslot * SLOTB, lane, it.x0, p.W, p.cmode, bv);
             // 8 rows; the row-validity test only in blocks with warm-up rows or rows past the band
+            // vertically reduced words of row r -> horizontal window -> one 16-byte store
+            auto emit = [&](uint8_t* d, const uint32_t* vmin, const uint32_t* vmax, const uint32_t* v) {
+                uint4 out;
+                if constexpr (MODE == MODE_GRAD) {
+                    // morphological gradient from one read: dilation - erosion. Bytes (u8) /
+                    // halves (u16) of max are >= those of min, so one 32-bit subtract per
+                    // word never borrows across pixels.
+                    const uint4 lo = ColCore<T, MODE_MIN, GX, GY>::horizontal(vmin, lane);
+                    const uint4 hi = ColCore<T, MODE_MAX, GX, GY>::horizontal(vmax, lane);
+                    out = make_uint4(hi.x - lo.x, hi.y - lo.y, hi.z - lo.z, hi.w - lo.w);
+                } else {
+                    out = C::horizontal(v, lane);
+                }
+                if (store_bytes == 16) *reinterpret_cast<uint4*>(d) = out;
+                else store_partial(d, out, store_bytes);
+            };
             auto block = [&](auto check_tag) {
                 constexpr bool CHECK = decltype(check_tag)::value;
+                if constexpr (WV >= 5) {
+                    // rows in pairs: the two vertical windows share WV - 1 rows (opn_pair)
 #pragma unroll
-                for (int r = 0; r < BR; ++r) {
-                    C::load_row(rows, r, lane, E[r % RING]);
-                    if (!CHECK || (unsigned)(o + r) < (unsigned)it.rows_out) {
-                        uint4 out;
-                        if constexpr (MODE == MODE_GRAD) {
-                            // morphological gradient from one read: dilation - erosion. Bytes (u8) /
-                            // halves (u16) of max are >= those of min, so one 32-bit subtract per
-                            // word never borrows across pixels.
-                            uint32_t vmin[NW], vmax[NW];
-#pragma unroll
-                            for (int w = 0; w < NW; ++w) {
-                                uint32_t col[WV];
-#pragma unroll
-                                for (int k = 0; k < WV; ++k) col[k] = E[(r - k + 8 * RING) % RING][w];
-                                vmin[w] = opn<MODE_MIN, WV>(col);
-                                vmax[w] = opn<MODE_MAX, WV>(col);
-                            }
-                            const uint4 lo = ColCore<T, MODE_MIN, GX, GY>::horizontal(vmin, lane);
-                            const uint4 hi = ColCore<T, MODE_MAX, GX, GY>::horizontal(vmax, lane);
-                            out = make_uint4(hi.x - lo.x, hi.y - lo.y, hi.z - lo.z, hi.w - lo.w);
-                        } else {
-                            uint32_t v[NW];
+                    for (int r = 0; r < BR; r += 2) {
+                        C::load_row(rows, r, lane, E[r % RING]);
+                        C::load_row(rows, r + 1, lane, E[(r + 1) % RING]);
+                        const bool ok0 = !CHECK || (unsigned)(o + r) < (unsigned)it.rows_out;
+                        const bool ok1 = !CHECK || (unsigned)(o + r + 1) < (unsigned)it.rows_out;
+                        if (ok0 || ok1) {
+                            uint32_t a0[NW], a1[NW], b0[NW], b1[NW];  // rows r / r + 1 (b*: max for the gradient)
 #pragma unroll
                             for (int w = 0; w < NW; ++w) {
-                                uint32_t col[WV];
+                                uint32_t col[WV + 1];  // rows r + 1, r, ..., r + 1 - WV
 #pragma unroll
-                                for (int k = 0; k < WV; ++k) col[k] = E[(r - k + 8 * RING) % RING][w];
-                                v[w] = opn<MODE, WV>(col);
+                                for (int k = 0; k <= WV; ++k) col[k] = E[(r + 1 - k + 8 * RING) % RING][w];
+                                if constexpr (MODE == MODE_GRAD) {
+                                    opn_pair<MODE_MIN, WV, 1>(col, a1[w], a0[w]);
+                                    opn_pair<MODE_MAX, WV, 1>(col, b1[w], b0[w]);
+                                } else {
+                                    opn_pair<MODE, WV, 1>(col, a1[w], a0[w]);
+                                }
                             }
-                            out = C::horizontal(v, lane);
+                            if (ok0) emit(drow, a0, b0, a0);
+                            if (ok1) emit(drow + dp, a1, b1, a1);
                         }
-                        if (store_bytes == 16) *reinterpret_cast<uint4*>(drow) = out;
-                        else store_partial(drow, out, store_bytes);
+                        drow += 2 * dp;
                     }
-                    drow += dp;
+                } else {
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        C::load_row(rows, r, lane, E[r % RING]);
+                        if (!CHECK || (unsigned)(o + r) < (unsigned)it.rows_out) {
+                            uint32_t a0[NW], b0[NW];
+#pragma unroll
+                            for (int w = 0; w < NW; ++w) {
+                                uint32_t col[WV];
+#pragma unroll
+                                for (int k = 0; k < WV; ++k) col[k] = E[(r - k + 8 * RING) % RING][w];
+                                if constexpr (MODE == MODE_GRAD) {
+                                    a0[w] = opn<MODE_MIN, WV>(col);
+                                    b0[w] = opn<MODE_MAX, WV>(col);
+                                } else {
+                                    a0[w] = opn<MODE, WV>(col);
+                                }
+                            }
+                            emit(drow, a0, b0, a0);
+                        }
+                        drow += dp;
+                    }
                 }
             };
             if (o >= 0 && o + BR <= it.rows_out) block(std::false_type{});
