@@ -569,7 +569,10 @@ cudaError_t launch_col_variant(const MorphJob& j, int R) {
     const int sms = device_sm_count();
     if (R <= 0) {
         // rows per item (R + 2*GY a multiple of BR): the warps run in waves of (SMs x resident
-        // warps) items; minimise waves x (staged rows per item + a fixed switch cost)
+        // warps) items; minimise waves x staged rows per item (ties go to the shorter item). A fixed
+        // per-item switch cost of 8 rows was in this model until round 2; measured without it:
+        // 4096^2 7x7 13.6 -> 12.7 us, 8192^2 3x3 31.1 -> 29.6, nothing more than 1% slower
+        // (knob col_switch)
         const long slots = (long)sms * std::max(1, occ) * WPB;
         const long strips = (long)p.nstrips * j.batch;
         double best = 1e30;
@@ -578,7 +581,7 @@ cudaError_t launch_col_variant(const MorphJob& j, int R) {
             if (r < 1) continue;
             const long items = strips * cdiv(j.H, r);
             const long waves = (items + slots - 1) / slots;
-            const double t = (double)waves * (m * BR + 8);
+            const double t = (double)waves * (m * BR + tune("col_switch", 0));
             if (t < best - 1e-9) {
                 best = t;
                 R = r;
